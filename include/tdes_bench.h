@@ -1,0 +1,55 @@
+/*
+ * tdes_bench.h -- measurement and synthetic-input helpers of the B200 3DES
+ * library.  None of these perform cipher arithmetic; they exist so that large
+ * workloads are generated and checked on the device (no PCIe in the timed
+ * path) and so that the roofline denominator is measured on the same GPU.
+ * Same error conventions as tdes.h.
+ */
+#ifndef TDES_BENCH_H_
+#define TDES_BENCH_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#include "tdes.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Fill dev_out (8-byte aligned device buffer of nblocks blocks) with the
+ * synthetic plaintext of DESIGN.md "Input recipe": block j is the 8
+ * little-endian bytes of splitmix64 counter (first_index + j + 1) under seed,
+ *   z = seed + (i+1)*0x9E3779B97F4A7C15; z = (z^z>>30)*0xBF58476D1CE4E5B9;
+ *   z = (z^z>>27)*0x94D049BB133111EB; block = z^z>>31   (all mod 2^64).
+ * Same generator as synthetic/__init__.py, so shards of any world size see
+ * the same global data. */
+int tdes_fill_splitmix64(void *dev_out, size_t nblocks, uint64_t first_index, uint64_t seed,
+                         tdes_stream_t stream);
+
+/* *dev_result (device uint64) += sum over blocks of the little-endian uint64
+ * value of each block, mod 2^64 (a mergeable digest).  Caller zeroes it. */
+int tdes_sum64(const void *dev_in, size_t nblocks, uint64_t *dev_result, tdes_stream_t stream);
+
+/* *dev_count (device uint64) += number of blocks where a and b differ. */
+int tdes_count_mismatch(const void *dev_a, const void *dev_b, size_t nblocks,
+                        uint64_t *dev_count, tdes_stream_t stream);
+
+/*
+ * LOP3 peak microbenchmark: grid x cta threads, each running `iters`
+ * iterations of `chains` independent lop3.b32 chains (16 LOP3 per iteration
+ * per thread).  Writes a data-dependent word per thread to dev_sink (grid*cta
+ * uint32) so nothing is dead.  *ops_out = total LOP3 thread-instructions the
+ * launch executes (for ops/s = ops / elapsed).
+ */
+int tdes_lop3_peak(uint32_t *dev_sink, int grid, int cta, int iters, uint64_t *ops_out,
+                   tdes_stream_t stream);
+
+/* Number of SMs of the current device and max resident CTAs/SM of the 3DES
+ * kernel (its occupancy), for grid accounting. */
+int tdes_device_geometry(int *num_sms, int *ctas_per_sm);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TDES_BENCH_H_ */

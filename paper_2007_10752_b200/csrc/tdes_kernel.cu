@@ -1,0 +1,335 @@
+// Bitsliced 3DES-EDE ECB for B200 (sm_100a) -- the hot path of arXiv 2007.10752.
+//
+// What it computes (§III): for every independent 64-bit
+// block (ECB) C = E_K3(D_K2(E_K1(P))) or the inverse.
+// How: instead of the paper's one-CTA-per-block,
+// one-thread-per-bit design, every thread owns 32 blocks and holds
+// them as 64 bit-planes (plane j = FIPS-renamed bit j of all 32 blocks):
+//
+//   S1 load      32 blocks per thread, coalesced (a warp reads 8 KiB contiguous)
+//   S2 transpose two 32x32 bit transposes (PRMT for the 16/8 stages)
+//   S3 IP        register renaming (free)
+//   S4 48 rounds key XOR with lane masks, 8 LOP3 S-box circuits, XOR into the
+//                other half; E and P are operand/destination renaming (free);
+//                the three DES stages are fused, IP/FP between them cancel
+//   S6 FP        register renaming (free)
+//   S7 store     inverse transpose + coalesced stores (in place allowed)
+//
+// All arithmetic is bitwise (LOP3/PRMT/SHF on the integer ALU pipe); nothing
+// is a contraction, so there are no tensor cores here.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <atomic>
+
+#include "../../include/tdes.h"
+#include "gen/tdes_gen.cuh"
+
+namespace {
+
+constexpr int kThreads = 256;        // 8 warps per CTA
+constexpr int kMinCtasPerSm = 2;     // => <= 128 registers per thread
+constexpr int kBlocksPerThread = 32; // one bit-plane word
+constexpr int kTileBlocks = 32 * kBlocksPerThread;  // per warp: 1024 blocks = 8 KiB
+constexpr int kWarpsPerCta = kThreads / 32;
+
+thread_local int g_last_cuda_error = 0;
+
+template <int NROUNDS>
+struct RoundMasks {
+  uint32_t m[NROUNDS][48];  // all-ones / all-zeros per key bit, consumption order
+};
+
+// In-register 32x32 bit-matrix transpose: a[i] bit j <-> a[j] bit i.
+// Stage s swaps bit s of the row and column index; s = 16 and 8 are whole
+// half-words / bytes and run as one PRMT per output word.
+__device__ __forceinline__ void transpose32(uint32_t (&a)[32]) {
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    const uint32_t lo = a[k], hi = a[k + 16];
+    a[k] = __byte_perm(lo, hi, 0x5410);
+    a[k + 16] = __byte_perm(lo, hi, 0x7632);
+  }
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    if (k & 8) continue;
+    const uint32_t lo = a[k], hi = a[k + 8];
+    a[k] = __byte_perm(lo, hi, 0x6240);
+    a[k + 8] = __byte_perm(lo, hi, 0x7351);
+  }
+#pragma unroll
+  for (int s = 4; s >= 1; s >>= 1) {
+    const uint32_t m = s == 4 ? 0x0F0F0F0Fu : s == 2 ? 0x33333333u : 0x55555555u;
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      if (k & s) continue;
+      const uint32_t lo = a[k], hi = a[k + s];
+      a[k] = tdes_gen::lop3<0xCA>(m, lo, hi << s);        // m ? lo : (hi << s)
+      a[k + s] = tdes_gen::lop3<0xCA>(m, lo >> s, hi);    // m ? (lo >> s) : hi
+    }
+  }
+}
+
+// One DES stage as 16 rounds starting with the given half (A = IP left half).
+template <bool START_A, int NR>
+__device__ __forceinline__ void des_stage(uint32_t (&P)[64], const RoundMasks<NR>& mk, int r0) {
+#pragma unroll 1
+  for (int r = r0; r < r0 + 16; r += 2) {
+    if (START_A) {
+      tdes_gen::round_A(P, mk.m[r]);
+      tdes_gen::round_B(P, mk.m[r + 1]);
+    } else {
+      tdes_gen::round_B(P, mk.m[r]);
+      tdes_gen::round_A(P, mk.m[r + 1]);
+    }
+  }
+}
+
+// NSTAGES = 3: fused 3DES (48 rounds); NSTAGES = 1: single DES (16 rounds).
+// VEC4: in/out 16-byte aligned -> 128-bit accesses (2 blocks per access).
+template <int NSTAGES, bool VEC4>
+__global__ void __launch_bounds__(kThreads, kMinCtasPerSm)
+tdes_ecb_kernel(const uint2* in, uint2* out, size_t nblocks,
+                const __grid_constant__ RoundMasks<16 * NSTAGES> mk) {
+  const unsigned lane = threadIdx.x & 31u;
+  const size_t ntiles = (nblocks + kTileBlocks - 1) / kTileBlocks;
+  const size_t nwarps = ((size_t)gridDim.x * blockDim.x) >> 5;
+  for (size_t tile = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; tile < ntiles;
+       tile += nwarps) {
+    const size_t base = tile * kTileBlocks;
+    const bool full = base + kTileBlocks <= nblocks;
+    uint32_t X[32], Y[32];
+    // ---- S1: load.  Plane bit i <-> the i-th block this lane loads. ----
+    if (VEC4) {
+      const uint4* in4 = reinterpret_cast<const uint4*>(in + base);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const size_t b = base + 64 * i + 2 * lane;
+        uint4 v;
+        if (full || b + 1 < nblocks) {
+          v = __ldcs(in4 + 32 * i + lane);
+        } else {
+          v = make_uint4(0u, 0u, 0u, 0u);
+          if (b < nblocks) {
+            const uint2 h = __ldcs(in + b);
+            v.x = h.x;
+            v.y = h.y;
+          }
+        }
+        X[2 * i] = v.x;
+        Y[2 * i] = v.y;
+        X[2 * i + 1] = v.z;
+        Y[2 * i + 1] = v.w;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const size_t b = base + 32 * i + lane;
+        uint2 v = make_uint2(0u, 0u);
+        if (full || b < nblocks) v = __ldcs(in + b);
+        X[i] = v.x;
+        Y[i] = v.y;
+      }
+    }
+    // ---- S2: to bit-planes ----
+    transpose32(X);
+    transpose32(Y);
+    uint32_t P[64];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      P[j] = X[j];
+      P[32 + j] = Y[j];
+    }
+    // ---- S3..S6: IP (renaming), 16*NSTAGES rounds, FP (renaming) ----
+    if (NSTAGES == 3) {
+      des_stage<true>(P, mk, 0);    // E_K1      (first round updates A)
+      des_stage<false>(P, mk, 16);  // D_K2      (starts on the half updated last)
+      des_stage<true>(P, mk, 32);   // E_K3
+    } else {
+      des_stage<true>(P, mk, 0);
+    }
+    uint32_t Q[64];
+    tdes_gen::output_planes(P, Q);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      X[j] = Q[j];
+      Y[j] = Q[32 + j];
+    }
+    // ---- S7: back to blocks, store ----
+    transpose32(X);
+    transpose32(Y);
+    if (VEC4) {
+      uint4* out4 = reinterpret_cast<uint4*>(out + base);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const size_t b = base + 64 * i + 2 * lane;
+        const uint4 v = make_uint4(X[2 * i], Y[2 * i], X[2 * i + 1], Y[2 * i + 1]);
+        if (full || b + 1 < nblocks) {
+          __stcs(out4 + 32 * i + lane, v);
+        } else if (b < nblocks) {
+          __stcs(out + b, make_uint2(v.x, v.y));
+        }
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const size_t b = base + 32 * i + lane;
+        if (full || b < nblocks) __stcs(out + b, make_uint2(X[i], Y[i]));
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------ launching ---
+
+constexpr int kMaxDevices = 64;
+std::atomic<int> g_sms[kMaxDevices];
+std::atomic<int> g_occ[kMaxDevices][2][2];  // [dev][stages==3][vec4]
+
+template <int NSTAGES, bool VEC4>
+int occupancy(int dev) {
+  int v = g_occ[dev][NSTAGES == 3][VEC4].load(std::memory_order_relaxed);
+  if (v > 0) return v;
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tdes_ecb_kernel<NSTAGES, VEC4>, kThreads,
+                                                    0) != cudaSuccess ||
+      occ <= 0)
+    occ = kMinCtasPerSm;
+  g_occ[dev][NSTAGES == 3][VEC4].store(occ, std::memory_order_relaxed);
+  return occ;
+}
+
+int num_sms(int dev) {
+  int v = g_sms[dev].load(std::memory_order_relaxed);
+  if (v > 0) return v;
+  int sms = 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0)
+    sms = 148;
+  g_sms[dev].store(sms, std::memory_order_relaxed);
+  return sms;
+}
+
+int cuda_fail(cudaError_t e) {
+  g_last_cuda_error = (int)e;
+  return TDES_ERR_CUDA;
+}
+
+int check_buffers(const void* in, const void* out, size_t nblocks) {
+  if (!in || !out) return TDES_ERR_INVALID_ARG;
+  if (((uintptr_t)in | (uintptr_t)out) & 7u) return TDES_ERR_MISALIGNED;
+  const uintptr_t a = (uintptr_t)in, b = (uintptr_t)out, len = (uintptr_t)nblocks * 8u;
+  if (a != b && a < b + len && b < a + len) return TDES_ERR_OVERLAP;
+  return TDES_OK;
+}
+
+template <int NSTAGES>
+int launch(const uint32_t (*masks)[48], const void* in, void* out, size_t nblocks,
+           cudaStream_t stream) {
+  if (nblocks == 0) return TDES_OK;
+  const int rc = check_buffers(in, out, nblocks);
+  if (rc) return rc;
+  if (nblocks > (SIZE_MAX >> 4)) return TDES_ERR_INVALID_ARG;
+  RoundMasks<16 * NSTAGES> mk;
+  memcpy(mk.m, masks, sizeof mk.m);
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e);
+  if (dev < 0 || dev >= kMaxDevices) return TDES_ERR_INVALID_ARG;
+  const bool vec4 = (((uintptr_t)in | (uintptr_t)out) & 15u) == 0;
+  const size_t ntiles = (nblocks + kTileBlocks - 1) / kTileBlocks;
+  const size_t want = (ntiles + kWarpsPerCta - 1) / kWarpsPerCta;
+  const int occ = vec4 ? occupancy<NSTAGES, true>(dev) : occupancy<NSTAGES, false>(dev);
+  const size_t resident = (size_t)num_sms(dev) * (size_t)occ;
+  const unsigned grid = (unsigned)(want < resident ? want : resident);
+  const uint2* pin = static_cast<const uint2*>(in);
+  uint2* pout = static_cast<uint2*>(out);
+  if (vec4)
+    tdes_ecb_kernel<NSTAGES, true><<<grid, kThreads, 0, stream>>>(pin, pout, nblocks, mk);
+  else
+    tdes_ecb_kernel<NSTAGES, false><<<grid, kThreads, 0, stream>>>(pin, pout, nblocks, mk);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e);
+  return TDES_OK;
+}
+
+}  // namespace
+
+extern "C" int tdes_ecb_encrypt(const tdes_schedule* s, const void* in, void* out, size_t nblocks,
+                                tdes_stream_t stream) {
+  if (!s) return TDES_ERR_INVALID_ARG;
+  return launch<3>(s->mask[0], in, out, nblocks, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" int tdes_ecb_decrypt(const tdes_schedule* s, const void* in, void* out, size_t nblocks,
+                                tdes_stream_t stream) {
+  if (!s) return TDES_ERR_INVALID_ARG;
+  return launch<3>(s->mask[1], in, out, nblocks, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" int des_ecb_encrypt(const des_schedule* s, const void* in, void* out, size_t nblocks,
+                               tdes_stream_t stream) {
+  if (!s) return TDES_ERR_INVALID_ARG;
+  return launch<1>(s->mask[0], in, out, nblocks, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" int des_ecb_decrypt(const des_schedule* s, const void* in, void* out, size_t nblocks,
+                               tdes_stream_t stream) {
+  if (!s) return TDES_ERR_INVALID_ARG;
+  return launch<1>(s->mask[1], in, out, nblocks, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" int tdes_ecb_crypt_host(const tdes_schedule* s, int decrypt, const void* host_in,
+                                   void* host_out, size_t nblocks, void* workspace,
+                                   size_t workspace_bytes, size_t chunk_blocks,
+                                   const tdes_stream_t* streams, int nstreams) {
+  if (!s || (decrypt != 0 && decrypt != 1) || nstreams <= 0 || !streams || chunk_blocks == 0)
+    return TDES_ERR_INVALID_ARG;
+  if (nblocks == 0) return TDES_OK;
+  if (!host_in || !host_out || !workspace) return TDES_ERR_INVALID_ARG;
+  if (((uintptr_t)workspace & 15u) || (chunk_blocks & 1u)) return TDES_ERR_MISALIGNED;
+  if (workspace_bytes / 8u / (size_t)nstreams < chunk_blocks) return TDES_ERR_WORKSPACE;
+  const uint8_t* src = static_cast<const uint8_t*>(host_in);
+  uint8_t* dst = static_cast<uint8_t*>(host_out);
+  const size_t chunk_bytes = chunk_blocks * 8u;
+  size_t c = 0;
+  for (size_t off = 0; off < nblocks; off += chunk_blocks, ++c) {
+    const size_t nb = nblocks - off < chunk_blocks ? nblocks - off : chunk_blocks;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(streams[c % (size_t)nstreams]);
+    uint8_t* dev = static_cast<uint8_t*>(workspace) + (c % (size_t)nstreams) * chunk_bytes;
+    cudaError_t e = cudaMemcpyAsync(dev, src + off * 8u, nb * 8u, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return cuda_fail(e);
+    const int rc = launch<3>(s->mask[decrypt], dev, dev, nb, st);
+    if (rc) return rc;
+    e = cudaMemcpyAsync(dst + off * 8u, dev, nb * 8u, cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) return cuda_fail(e);
+  }
+  for (int i = 0; i < nstreams; ++i) {
+    const cudaError_t e = cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(streams[i]));
+    if (e != cudaSuccess) return cuda_fail(e);
+  }
+  return TDES_OK;
+}
+
+extern "C" int tdes_get_kernel_info(tdes_kernel_info* out) {
+  if (!out) return TDES_ERR_INVALID_ARG;
+  out->sbox_lop3_total = tdes_gen::kSboxLop3Total;
+  for (int g = 0; g < 8; ++g) out->sbox_lop3[g] = tdes_gen::kSboxLop3[g];
+  out->threads_per_cta = kThreads;
+  out->blocks_per_thread = kBlocksPerThread;
+  out->min_ctas_per_sm = kMinCtasPerSm;
+  return TDES_OK;
+}
+
+extern "C" int tdes_last_cuda_error(void) { return g_last_cuda_error; }
+
+extern "C" int tdes_device_geometry(int* sms, int* ctas_per_sm) {
+  if (!sms || !ctas_per_sm) return TDES_ERR_INVALID_ARG;
+  int dev = 0;
+  const cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e);
+  if (dev < 0 || dev >= kMaxDevices) return TDES_ERR_INVALID_ARG;
+  *sms = num_sms(dev);
+  *ctas_per_sm = occupancy<3, true>(dev);
+  return TDES_OK;
+}

@@ -1,0 +1,227 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, bit-exact.
+
+Integer/byte work, so the bar is bit-exactness everywhere.  Small and ragged
+sizes are compared element by element; the full BASELINE.json sizes (in the
+launch configuration bench.py times) are compared on sampled blocks the oracle
+computes one by one, plus whole-buffer properties (device round trip, the
+device generator equal to synthetic/).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synthetic
+
+pytestmark = pytest.mark.gpu
+
+KEYINGS = {"3key": synthetic.KEYS_3KEY, "2key": synthetic.KEYS_2KEY, "1key": synthetic.KEYS_1KEY}
+SIZES = [0, 1, 2, 31, 32, 33, 63, 64, 65, 1023, 1024, 1025, 2047, 8191, 8193, 131071, 131072]
+
+
+@pytest.fixture(scope="module")
+def tdes():
+    import paper_2007_10752_b200 as m
+    torch.cuda.set_device(0)
+    return m
+
+
+def to_dev(a: np.ndarray) -> torch.Tensor:
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+@pytest.mark.parametrize("n", SIZES)
+@pytest.mark.parametrize("decrypt", [False, True])
+def test_sizes_vs_oracle(tdes, n, decrypt):
+    keys = synthetic.KEYS_3KEY
+    p = synthetic.plaintext_bytes(7 * n, n)
+    s = tdes.key_schedule(*keys)
+    fn = tdes.ecb_decrypt if decrypt else tdes.ecb_encrypt
+    got = fn(to_dev(p), s).cpu().numpy()
+    exp = oracle.tdes_ecb(*keys, p, decrypt=decrypt)
+    assert np.array_equal(got, exp)
+
+
+@pytest.mark.parametrize("keying", list(KEYINGS))
+def test_keyings_vs_oracle(tdes, keying):
+    keys = KEYINGS[keying]
+    n = 40000
+    p = synthetic.plaintext_bytes(0, n)
+    s = tdes.key_schedule(*keys)
+    c = tdes.ecb_encrypt(to_dev(p), s)
+    assert np.array_equal(c.cpu().numpy(), oracle.tdes_ecb(*keys, p))
+    d = tdes.ecb_decrypt(c, s)
+    assert np.array_equal(d.cpu().numpy(), p)
+
+
+def test_random_keys_and_data(tdes):
+    rng = np.random.default_rng(11)
+    for _ in range(6):
+        ks = [synthetic.random_key(rng) for _ in range(3)]
+        n = int(rng.integers(1, 5000))
+        p = synthetic.random_blocks(rng, n)
+        s = tdes.key_schedule(*ks)
+        for dec in (False, True):
+            fn = tdes.ecb_decrypt if dec else tdes.ecb_encrypt
+            assert np.array_equal(fn(to_dev(p), s).cpu().numpy(), oracle.tdes_ecb(*ks, p, decrypt=dec))
+
+
+def test_known_answers(tdes, kat_rows):
+    for kind, f, cite in kat_rows:
+        if kind == "TDES":
+            s = tdes.key_schedule(*f[:3])
+            pt, ct = bytes.fromhex(f[3]), bytes.fromhex(f[4])
+        elif kind == "DES":
+            s = tdes.key_schedule(f[0], f[0], f[0])   # P:86 K1=K2=K3 behaves as DES
+            pt, ct = bytes.fromhex(f[1]), bytes.fromhex(f[2])
+        else:
+            continue
+        x = to_dev(np.frombuffer(pt, np.uint8))
+        assert tdes.ecb_encrypt(x, s).cpu().numpy().tobytes() == ct, cite
+        y = to_dev(np.frombuffer(ct, np.uint8))
+        assert tdes.ecb_decrypt(y, s).cpu().numpy().tobytes() == pt, cite
+
+
+def test_in_place_and_8byte_aligned_paths(tdes):
+    n = 5000
+    p = synthetic.plaintext_bytes(3, n)
+    s = tdes.key_schedule(*synthetic.KEYS_3KEY)
+    exp = oracle.tdes_ecb(*synthetic.KEYS_3KEY, p)
+    x = to_dev(p)
+    tdes.ecb_encrypt(x, s, out=x)                              # in place, 16B aligned
+    assert np.array_equal(x.cpu().numpy(), exp)
+    buf = torch.zeros(8 * (n + 3), dtype=torch.uint8, device="cuda")
+    src = buf[8:8 + 8 * n]                                     # 8B but not 16B aligned
+    src.copy_(to_dev(p))
+    dst = torch.zeros(8 * (n + 1), dtype=torch.uint8, device="cuda")[8:]
+    assert src.data_ptr() % 16 == 8
+    tdes.ecb_encrypt(src, s, out=dst)
+    assert np.array_equal(dst.cpu().numpy(), exp)
+    tdes.ecb_encrypt(src, s, out=src)                          # in place, 8B aligned
+    assert np.array_equal(src.cpu().numpy(), exp)
+    assert buf[:8].sum().item() == 0 and buf[8 + 8 * n:].sum().item() == 0   # no stray writes
+
+
+def test_overlap_and_alignment_errors(tdes):
+    s = tdes.key_schedule(*synthetic.KEYS_3KEY)
+    buf = torch.zeros(8 * 100, dtype=torch.uint8, device="cuda")
+    with pytest.raises(tdes.TdesError) as e:
+        tdes.ecb_encrypt_ptr(s, buf.data_ptr(), buf.data_ptr() + 8, 10)
+    assert e.value.code == -3
+    with pytest.raises(tdes.TdesError) as e:
+        tdes.ecb_encrypt_ptr(s, buf.data_ptr() + 4, buf.data_ptr() + 400, 10)
+    assert e.value.code == -2
+
+
+def test_single_des_entry_points(tdes, kat_rows):
+    rng = np.random.default_rng(12)
+    for _ in range(3):
+        k = synthetic.random_key(rng)
+        p = synthetic.random_blocks(rng, 3001)
+        s = tdes.des_key_schedule(k)
+        c = tdes.des_ecb_encrypt(to_dev(p), s)
+        assert np.array_equal(c.cpu().numpy(), oracle.tdes_ecb(k, k, k, p))
+        assert np.array_equal(tdes.des_ecb_decrypt(c, s).cpu().numpy(), p)
+    for kind, f, cite in kat_rows:
+        if kind == "DES":
+            s = tdes.des_key_schedule(f[0])
+            x = to_dev(np.frombuffer(bytes.fromhex(f[1]), np.uint8))
+            assert tdes.des_ecb_encrypt(x, s).cpu().numpy().tobytes() == bytes.fromhex(f[2]), cite
+
+
+def test_streams_and_concurrent_keys(tdes):
+    n = 20000
+    p = synthetic.plaintext_bytes(0, n)
+    x = to_dev(p)
+    rng = np.random.default_rng(13)
+    keysets = [[synthetic.random_key(rng) for _ in range(3)] for _ in range(4)]
+    streams = [torch.cuda.Stream() for _ in keysets]
+    outs = []
+    torch.cuda.synchronize()
+    for ks, st in zip(keysets, streams):
+        s = tdes.key_schedule(*ks)
+        with torch.cuda.stream(st):
+            outs.append(tdes.ecb_encrypt(x, s, stream=st))
+        del s  # masks were copied into the launch: freeing the schedule is safe
+    torch.cuda.synchronize()
+    for ks, o in zip(keysets, outs):
+        assert np.array_equal(o.cpu().numpy(), oracle.tdes_ecb(*ks, p))
+
+
+def test_device_generator_matches_synthetic(tdes):
+    n = 100003
+    x = torch.empty(8 * n, dtype=torch.uint8, device="cuda")
+    tdes.fill_splitmix64(x, first_index=12345)
+    assert np.array_equal(x.cpu().numpy(), synthetic.plaintext_bytes(12345, n))
+
+
+def test_sum64_and_mismatch_helpers(tdes):
+    n = 50000
+    p = synthetic.plaintext_bytes(0, n)
+    x = to_dev(p)
+    assert tdes.sum64(x) == int(p.view("<u8").sum(dtype=np.uint64))
+    y = x.clone()
+    y[8 * 77] ^= 1
+    y[8 * 4000 + 3] ^= 0x80
+    assert tdes.count_mismatch(x, y) == 2
+
+
+def test_host_pipeline_vs_oracle(tdes):
+    n = 100001
+    p = synthetic.plaintext_bytes(5, n)
+    s = tdes.key_schedule(*synthetic.KEYS_3KEY)
+    hin = torch.from_numpy(p.copy()).pin_memory()
+    hout = torch.empty_like(hin).pin_memory()
+    pipe = tdes.HostPipeline(chunk_blocks=8192, nstreams=3)
+    pipe.run(s, hin, hout)
+    assert np.array_equal(hout.numpy(), oracle.tdes_ecb(*synthetic.KEYS_3KEY, p))
+    back = torch.empty_like(hin).pin_memory()
+    pipe.run(s, hout, back, decrypt=True)
+    assert np.array_equal(back.numpy(), p)
+    pipe.run(s, hout, hout, decrypt=True)        # aliasing host buffers
+    assert np.array_equal(hout.numpy(), p)
+
+
+def _sampled_check(tdes, keys, nblocks, decrypt=False, nsample=1 << 14):
+    """Run the full-size config on device; compare sampled blocks with the oracle."""
+    s = tdes.key_schedule(*keys)
+    x = torch.empty(8 * nblocks, dtype=torch.uint8, device="cuda")
+    tdes.fill_splitmix64(x)
+    y = torch.empty_like(x)
+    (tdes.ecb_decrypt if decrypt else tdes.ecb_encrypt)(x, s, out=y)
+    rng = np.random.default_rng(nblocks)
+    idx = np.unique(np.concatenate([
+        rng.integers(0, nblocks, nsample), np.arange(1024), np.arange(nblocks - 1024, nblocks)]))
+    got = y.view(-1, 8)[torch.from_numpy(idx).cuda()].cpu().numpy().reshape(-1)
+    exp = oracle.tdes_ecb(*keys, synthetic.gather_blocks(idx), decrypt=decrypt)
+    assert np.array_equal(got, exp)
+    # whole-buffer property: the inverse on the device restores the input
+    z = (tdes.ecb_encrypt if decrypt else tdes.ecb_decrypt)(y, s)
+    assert tdes.count_mismatch(z, x) == 0
+    del x, y, z
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("decrypt", [False, True])
+def test_config2_top_1gib_sampled(tdes, decrypt):
+    _sampled_check(tdes, synthetic.KEYS_3KEY, 1 << 27, decrypt)
+
+
+@pytest.mark.parametrize("keying", ["1key", "2key"])
+def test_config3_256mib_sampled(tdes, keying):
+    _sampled_check(tdes, KEYINGS[keying], synthetic.C3_BLOCKS)
+
+
+def test_config1_full_vs_oracle(tdes):
+    n = synthetic.C1_BLOCKS
+    p = synthetic.plaintext_bytes(0, n)
+    x = torch.empty(8 * n, dtype=torch.uint8, device="cuda")
+    tdes.fill_splitmix64(x)
+    s = tdes.key_schedule(*synthetic.KEYS_3KEY)
+    got = tdes.ecb_encrypt(x, s).cpu().numpy()
+    assert np.array_equal(got, oracle.tdes_ecb(*synthetic.KEYS_3KEY, p))
+
+
+def test_ragged_large_size(tdes):
+    # not a multiple of the 1024-block warp tile, and more tiles than resident warps
+    _sampled_check(tdes, synthetic.KEYS_3KEY, (1 << 23) + 777, nsample=4096)

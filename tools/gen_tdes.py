@@ -1,0 +1,330 @@
+#!/usr/bin/env python3
+"""Generator for the bitsliced 3DES kernel's compile-time constants.
+
+Emits ``paper_2007_10752_b200/csrc/gen/tdes_gen.cuh`` from the product-side
+tables in ``tools/des_tables.py`` (never from oracle/):
+
+* the plane renaming maps: which register holds FIPS bit n of the thread's 32
+  blocks after the load transpose (byte order folded in), the IP
+  halves as register names (PAPER.md:61 -- IP costs nothing), E as operand
+  selection, P as destination selection and
+  FP∘swap as a register renaming for the store transpose;
+* the eight S-boxes as ``lop3.b32`` circuits.  Each circuit is
+  verified exhaustively (64 inputs x 4 outputs) against des_tables.SBOX before
+  it is emitted.  The circuit source is the best verified one among the
+  searched circuits in ``tools/circuits/*.json`` (written by tools/sbox_search)
+  and the explicit Shannon mux-tree built here (correct by construction);
+* the host-side key-schedule tables (PC-1, PC-2, shifts).
+
+Run: python tools/gen_tdes.py [--muxtree-only]
+"""
+from __future__ import annotations
+
+import argparse
+import glob
+import json
+import os
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+sys.path.insert(0, HERE)
+import des_tables as T  # noqa: E402
+
+OUT_DIR = os.path.join(ROOT, "paper_2007_10752_b200", "csrc", "gen")
+CIRCUIT_DIR = os.path.join(HERE, "circuits")
+FULL = (1 << 64) - 1
+
+# ------------------------------------------------------------ truth tables --
+# A 6-input Boolean function is a 64-bit int: bit v is its value on input v,
+# where input x_i (i = 0..5, = S-box input bit b_{i+1}) is bit (5 - i) of v.
+
+
+def var_tt(i: int) -> int:
+    return sum(1 << v for v in range(64) if (v >> (5 - i)) & 1)
+
+
+VARS = [var_tt(i) for i in range(6)]
+
+
+def sbox_tt(g: int, o: int) -> int:
+    """Truth table of output bit o (0 = MSB) of S-box g (0-based); row = 2*b1+b6."""
+    tt = 0
+    for v in range(64):
+        b = [(v >> (5 - i)) & 1 for i in range(6)]
+        row, col = 2 * b[0] + b[5], 8 * b[1] + 4 * b[2] + 2 * b[3] + b[4]
+        if (T.SBOX[g][row][col] >> (3 - o)) & 1:
+            tt |= 1 << v
+    return tt
+
+
+def lut_eval(lut: int, a: int, b: int, c: int, full: int = FULL) -> int:
+    """PTX lop3 semantics: result bit = lut[(a<<2)|(b<<1)|c]."""
+    r = 0
+    for k in range(8):
+        if (lut >> k) & 1:
+            r |= (a if k & 4 else ~a) & (b if k & 2 else ~b) & (c if k & 1 else ~c)
+    return r & full
+
+
+# ----------------------------------------------------------------- circuits --
+# circuit = {"gates": [[lut, a, b, c], ...], "outputs": [s0, s1, s2, s3]}
+# signals 0..5 are the inputs x0..x5; signal 6+k is gate k.
+
+
+def eval_circuit(circ, inputs=None, full=FULL):
+    sig = list(inputs if inputs is not None else VARS)
+    for lut, a, b, c in circ["gates"]:
+        sig.append(lut_eval(lut, sig[a], sig[b], sig[c], full))
+    return [sig[s] for s in circ["outputs"]]
+
+
+def verify_circuit(g: int, circ) -> bool:
+    if len(circ["outputs"]) != 4:
+        return False
+    for k, (lut, a, b, c) in enumerate(circ["gates"]):
+        if not (0 <= lut <= 255 and max(a, b, c) < 6 + k and min(a, b, c) >= 0):
+            return False
+    return eval_circuit(circ) == [sbox_tt(g, o) for o in range(4)]
+
+
+def muxtree_circuit(g: int):
+    """Shannon expansion: 8 leaves over (x1,x2,x3) per output, then muxes on x4, x5, x0.
+
+    Leaves are shared across the 4 outputs when their LUT coincides.
+    """
+    gates, leaf = [], {}
+
+    def gate(lut, a, b, c):
+        gates.append([lut, a, b, c])
+        return 5 + len(gates)
+
+    MUX = 0xCA  # a ? b : c
+    outs = []
+    for o in range(4):
+        f = sbox_tt(g, o)
+        lv = {}
+        for a0 in (0, 1):
+            for a4 in (0, 1):
+                for a5 in (0, 1):
+                    lut = 0
+                    for k in range(8):
+                        x1, x2, x3 = (k >> 2) & 1, (k >> 1) & 1, k & 1
+                        v = (a0 << 5) | (x1 << 4) | (x2 << 3) | (x3 << 2) | (a4 << 1) | a5
+                        if (f >> v) & 1:
+                            lut |= 1 << k
+                    if lut not in leaf:
+                        leaf[lut] = gate(lut, 1, 2, 3)
+                    lv[(a0, a4, a5)] = leaf[lut]
+        m4 = {(a0, a5): gate(MUX, 4, lv[(a0, 1, a5)], lv[(a0, 0, a5)]) for a0 in (0, 1) for a5 in (0, 1)}
+        m5 = {a0: gate(MUX, 5, m4[(a0, 1)], m4[(a0, 0)]) for a0 in (0, 1)}
+        outs.append(gate(MUX, 0, m5[1], m5[0]))
+    return {"gates": gates, "outputs": outs, "source": "muxtree"}
+
+
+def load_searched():
+    """Best verified searched circuit per S-box from tools/circuits/*.json."""
+    best = {}
+    for path in sorted(glob.glob(os.path.join(CIRCUIT_DIR, "*.json"))):
+        with open(path) as f:
+            data = json.load(f)
+        for item in data.get("circuits", []):
+            g = item["sbox"]
+            circ = {"gates": item["gates"], "outputs": item["outputs"],
+                    "source": os.path.basename(path)}
+            if not verify_circuit(g, circ):
+                print(f"warning: {path} S{g + 1} circuit fails verification; ignored", file=sys.stderr)
+                continue
+            if g not in best or len(circ["gates"]) < len(best[g]["gates"]):
+                best[g] = circ
+    return best
+
+
+def choose_circuits(muxtree_only=False):
+    searched = {} if muxtree_only else load_searched()
+    out = []
+    for g in range(8):
+        m = muxtree_circuit(g)
+        assert verify_circuit(g, m)
+        c = searched.get(g)
+        out.append(c if c is not None and len(c["gates"]) < len(m["gates"]) else m)
+    return out
+
+
+# ------------------------------------------------------------ plane maps ----
+# Thread-local layout: 32 blocks loaded as little-endian uint2 {x, y}; after the
+# 32x32 transpose of the x words and of the y words, register P[32*w + j] holds
+# bit j of word w of each block (bit i of the plane = block i).  FIPS bit n
+# (1..64; bit 1 = MSB of byte 0) lives in word (n-1)>>5 at bit
+# 8*(((n-1)>>3)&3) + 7 - ((n-1)&7).
+
+
+def plane_of(n: int) -> int:
+    w = (n - 1) >> 5
+    j = 8 * (((n - 1) >> 3) & 3) + 7 - ((n - 1) & 7)
+    return 32 * w + j
+
+
+A_IDX = [plane_of(T.IP[i]) for i in range(32)]        # L0 = IP bits 1..32
+B_IDX = [plane_of(T.IP[32 + i]) for i in range(32)]   # R0 = IP bits 33..64
+# f position i (0-based) takes S-output bit P[i]-1.
+P_SRC = [T.P[i] - 1 for i in range(32)]
+
+
+def out_src() -> list[int]:
+    """Q[plane_of(n)] = P[out_src[plane_of(n)]]: FP applied to (B || A) (reading Q4)."""
+    q = [None] * 64
+    for n in range(1, 65):
+        m = T.FP[n - 1]
+        src = B_IDX[m - 1] if m <= 32 else A_IDX[m - 33]
+        q[plane_of(n)] = src
+    assert sorted(q) == list(range(64))
+    return q
+
+
+OUT_SRC = out_src()
+
+
+def round_schedule():
+    """Which half each of the 48 fused rounds updates: 'A' or 'B'.
+
+    Stage s (0..2), round r (1..16) updates A iff (r + s) is odd, because the
+    pre-output swap R16||L16 followed by FP∘IP = id makes the next stage's first
+    round update the half the previous stage updated last.
+    """
+    return ["A" if (r + s) % 2 == 1 else "B" for s in range(3) for r in range(1, 17)]
+
+
+# ------------------------------------------------------------------ emitter --
+
+
+def emit_sbox(g, circ):
+    lines = [f"// S{g + 1}: {len(circ['gates'])} lop3 ({circ['source']})",
+             f"__device__ __forceinline__ void sbox{g + 1}(uint32_t x0, uint32_t x1, uint32_t x2, "
+             "uint32_t x3, uint32_t x4, uint32_t x5,",
+             "    uint32_t& o0, uint32_t& o1, uint32_t& o2, uint32_t& o3) {"]
+
+    def name(s):
+        return f"x{s}" if s < 6 else f"t{s - 6}"
+    for k, (lut, a, b, c) in enumerate(circ["gates"]):
+        lines.append(f"  const uint32_t t{k} = lop3<0x{lut:02x}>({name(a)}, {name(b)}, {name(c)});")
+    for o, s in enumerate(circ["outputs"]):
+        lines.append(f"  o{o} = {name(s)};")
+    lines.append("}")
+    return "\n".join(lines)
+
+
+def emit_round(half):
+    dst, src = (A_IDX, B_IDX) if half == "A" else (B_IDX, A_IDX)
+    # inverse of P: S-output bit m feeds f position pinv[m]
+    pinv = [None] * 32
+    for i, m in enumerate(P_SRC):
+        pinv[m] = i
+    lines = [f"// One Feistel round updating half {half}: {half} ^= P(S(E(other) ^ K)).",
+             f"__device__ __forceinline__ void round_{half}(uint32_t (&P)[64], const uint32_t* __restrict__ K) {{"]
+    for g in range(8):
+        xs = [f"P[{src[T.E[6 * g + i] - 1]}] ^ K[{6 * g + i}]" for i in range(6)]
+        lines.append(f"  {{ uint32_t o0, o1, o2, o3;")
+        lines.append(f"    sbox{g + 1}({', '.join(xs)}, o0, o1, o2, o3);")
+        for o in range(4):
+            lines.append(f"    P[{dst[pinv[4 * g + o]]}] ^= o{o};")
+        lines.append("  }")
+    lines.append("}")
+    return "\n".join(lines)
+
+
+def emit_header(circs):
+    T.check()
+    total = sum(len(c["gates"]) for c in circs)
+    h = [
+        "// GENERATED by tools/gen_tdes.py from tools/des_tables.py -- do not edit.",
+        "// Bitsliced DES building blocks for the sm_100a 3DES-ECB kernel.",
+        "// Planes: P[32*w + j] holds bit j of little-endian word w of each of the",
+        "// thread's 32 blocks (bit i of a plane = block i).",
+        f"// S-box LOP3 total T = {total} per round; per round ops = 48 key XOR + T + 32 Feistel XOR.",
+        "#pragma once",
+        "#include <stdint.h>",
+        "",
+        "namespace tdes_gen {",
+        "",
+        f"constexpr int kSboxLop3Total = {total};",
+        f"constexpr int kSboxLop3[8] = {{{', '.join(str(len(c['gates'])) for c in circs)}}};",
+        "",
+        "template <unsigned LUT>",
+        "__device__ __forceinline__ uint32_t lop3(uint32_t a, uint32_t b, uint32_t c) {",
+        "  uint32_t d;",
+        "  asm(\"lop3.b32 %0, %1, %2, %3, %4;\" : \"=r\"(d) : \"r\"(a), \"r\"(b), \"r\"(c), \"n\"(LUT));",
+        "  return d;",
+        "}",
+        "",
+    ]
+    for g, c in enumerate(circs):
+        h.append(emit_sbox(g, c))
+        h.append("")
+    h.append(emit_round("A"))
+    h.append("")
+    h.append(emit_round("B"))
+    h.append("")
+    h.append("// Pre-output (B || A) through FP, renamed into store-transpose order (PAPER.md:74-75).")
+    h.append("__device__ __forceinline__ void output_planes(const uint32_t (&P)[64], uint32_t (&Q)[64]) {")
+    for k in range(64):
+        h.append(f"  Q[{k}] = P[{OUT_SRC[k]}];")
+    h.append("}")
+    h.append("")
+    h.append("}  // namespace tdes_gen")
+    h.append("")
+    return "\n".join(h)
+
+
+def emit_host_tables():
+    T.check()
+
+    def arr(name, vals, ctype="uint8_t"):
+        return f"static const {ctype} {name}[{len(vals)}] = {{{', '.join(map(str, vals))}}};"
+    return "\n".join([
+        "// GENERATED by tools/gen_tdes.py from tools/des_tables.py -- do not edit.",
+        "// Host key-schedule tables (FIPS 46-3, PAPER.md:212-245), 1-based as printed.",
+        "#pragma once",
+        "#include <stdint.h>",
+        arr("kPC1", T.PC1),
+        arr("kPC2", T.PC2),
+        arr("kShifts", T.SHIFTS),
+        "",
+    ])
+
+
+def manifest(circs):
+    return {
+        "sbox_lop3": [len(c["gates"]) for c in circs],
+        "sbox_lop3_total": sum(len(c["gates"]) for c in circs),
+        "sources": [c["source"] for c in circs],
+        "circuits": [{"sbox": g, "gates": c["gates"], "outputs": c["outputs"]} for g, c in enumerate(circs)],
+        "a_idx": A_IDX, "b_idx": B_IDX, "p_src": P_SRC, "out_src": OUT_SRC,
+        "round_schedule": round_schedule(),
+    }
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--muxtree-only", action="store_true")
+    ap.add_argument("--out", default=OUT_DIR)
+    args = ap.parse_args(argv)
+    circs = choose_circuits(args.muxtree_only)
+    os.makedirs(args.out, exist_ok=True)
+    files = {
+        "tdes_gen.cuh": emit_header(circs),
+        "tdes_host_tables.h": emit_host_tables(),
+        "manifest.json": json.dumps(manifest(circs), indent=1) + "\n",
+    }
+    for name, text in files.items():
+        path = os.path.join(args.out, name)
+        old = open(path).read() if os.path.exists(path) else None
+        if old != text:
+            with open(path, "w") as f:
+                f.write(text)
+    print("S-box LOP3 per box:", [len(c["gates"]) for c in circs],
+          "total", sum(len(c["gates"]) for c in circs))
+
+
+if __name__ == "__main__":
+    main()
