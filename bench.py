@@ -1,0 +1,407 @@
+#!/usr/bin/env python3
+"""Benchmark of the bitsliced 3DES-EDE ECB hot path (arXiv 2007.10752) on B200.
+
+Workload (BASELINE.json configs[1], top of the paper-style size sweep): 3DES-EDE
+ECB **encrypt** of 2^27 blocks = 1 GiB of synthetic plaintext per GPU, 3-key
+(NIST SP 800-67 sample keys).  One step = one pass of the whole hot path (one
+fused kernel launch: load, transpose, 48 rounds, transpose, store) over the
+1 GiB batch.  Inputs (1 GiB) and outputs (1 GiB) exceed the 126 MB L2, so no
+flush is needed between steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 runs under torchrun, one process per GPU, each rank encrypting its own
+1 GiB block-range shard of the global data (weak scaling, no collective on the
+data path; NCCL only for the barrier and the max-over-ranks time).
+
+``--impl reference`` times the CPU oracle (oracle/, the literal char-per-bit
+C implementation, OpenMP over blocks as in the paper's CPU baseline)
+on a bounded sample of the same workload; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synthetic  # noqa: E402
+
+METRIC = "3DES-ECB encrypt GB/s per B200 and at 1/2/4/8 GPUs; % of INT32/LOP3 roofline"
+UNIT = "GB/s"
+BLOCKS_PER_GPU = 1 << 27          # 1 GiB per GPU
+WORKLOAD = "3DES-EDE ECB encrypt, 1 GiB (2^27 blocks) per GPU, 3-key (SP 800-67 sample keys), synthetic splitmix64 plaintext"
+SM_COUNT_NOMINAL = 148
+LOP3_LANES_PER_SM = 64            # B300_MICROARCH.md: LOP3 on the alu pipe, rt_SMSP = 2 -> 16 lanes/clk/SMSP
+HBM_PEAK_FALLBACK = 6650.0        # B200_PROFILING.md fallback (GB/s)
+
+
+def env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+def read_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except (OSError, ValueError):
+        return {"hbm_gbs": HBM_PEAK_FALLBACK, "sm_max_mhz": 1965.0}, "fallback"
+
+
+def read_traffic():
+    """Per-block DRAM bytes of the kernel from the committed ncu capture, if any."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["dram_bytes_per_block"]), d.get("source", path)
+    except (OSError, ValueError, KeyError):
+        return None, None
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons via NVML every ~10 ms while running."""
+
+    def __init__(self, pci_bus_id, fallback_index):
+        self.samples, self.reasons, self.ok = [], set(), False
+        self.max_mhz = None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = None
+            for bus in ([pci_bus_id, "0000" + pci_bus_id] if pci_bus_id else []):
+                try:
+                    self.h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+                    break
+                except Exception:
+                    pass
+            if self.h is None:
+                self.h = pynvml.nvmlDeviceGetHandleByIndex(fallback_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.ok = False
+        self.names = {}
+        if self.ok:
+            for attr, name in [("nvmlClocksEventReasonGpuIdle", "gpu_idle"),
+                               ("nvmlClocksEventReasonApplicationsClocksSetting", "applications_clocks_setting"),
+                               ("nvmlClocksEventReasonSwPowerCap", "sw_power_cap"),
+                               ("nvmlClocksEventReasonHwSlowdown", "hw_slowdown"),
+                               ("nvmlClocksEventReasonSyncBoost", "sync_boost"),
+                               ("nvmlClocksEventReasonSwThermalSlowdown", "sw_thermal_slowdown"),
+                               ("nvmlClocksEventReasonHwThermalSlowdown", "hw_thermal_slowdown"),
+                               ("nvmlClocksEventReasonHwPowerBrakeSlowdown", "hw_power_brake_slowdown")]:
+                v = getattr(self.nv, attr, None)
+                if v is None:
+                    v = getattr(self.nv, attr.replace("ClocksEvent", "ClocksThrottle"), None)
+                if v is not None:
+                    self.names[v] = name
+
+    def _run(self):
+        nv = self.nv
+        get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = get_reasons(self.h)
+                for bit, name in self.names.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.01)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml_unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "sm_mhz_min": min(self.samples), "samples": len(self.samples),
+                "reasons": sorted(self.reasons)}
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def oracle_rate(budget_s: float, max_blocks: int):
+    """Time the oracle (as it stands) on a bounded sample of the workload.
+
+    Returns (GB/s, threads used, sample description, seconds)."""
+    import oracle
+    keys = synthetic.KEYS_3KEY
+    probe = 1 << 12
+    p = synthetic.plaintext_bytes(0, probe)
+    out = np.empty_like(p)
+    t0 = time.perf_counter()
+    oracle.tdes_ecb_into(*keys, p, out)
+    dt = max(time.perf_counter() - t0, 1e-6)
+    n = int(min(max_blocks, max(probe, budget_s * probe / dt)))
+    n -= n % 1024
+    p = synthetic.plaintext_bytes(0, n)
+    out = np.empty_like(p)
+    t0 = time.perf_counter()
+    used = oracle.tdes_ecb_into(*keys, p, out)
+    dt = time.perf_counter() - t0
+    return n * 8 / dt / 1e9, used, f"first {n} blocks ({n * 8 / 2**20:.1f} MiB) of the workload, wall clock, OpenMP over blocks", dt
+
+
+# ------------------------------------------------------------ reference arm --
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    import oracle
+    keys = synthetic.KEYS_3KEY
+    # size each step so the whole --steps K --warmup W run ends within ~2 minutes
+    probe = 1 << 12
+    p = synthetic.plaintext_bytes(0, probe)
+    out = np.empty_like(p)
+    t0 = time.perf_counter()
+    oracle.tdes_ecb_into(*keys, p, out)
+    dt = max(time.perf_counter() - t0, 1e-6)
+    per_step_s = min(10.0, 120.0 / max(1, args.steps + args.warmup))
+    n = int(max(1024, min(BLOCKS_PER_GPU, per_step_s * probe / dt)))
+    n -= n % 1024
+    p = synthetic.plaintext_bytes(0, n)
+    out = np.empty_like(p)
+    used = 1
+    for _ in range(args.warmup):
+        used = oracle.tdes_ecb_into(*keys, p, out)
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        used = oracle.tdes_ecb_into(*keys, p, out)
+        ts.append(time.perf_counter() - t0)
+    total = sum(ts)
+    value = args.steps * n * 8 / total / 1e9
+    sample = f"first {n} blocks ({n * 8 / 2**20:.2f} MiB) of the 1 GiB workload per step, wall clock"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic",
+        "config": {"workload": WORKLOAD + " (oracle timed on a bounded sample)", "blocks_per_step": n,
+                   "parallelism": "OpenMP over blocks on host cores (PAPER.md:140)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": used, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------- our arm --
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    import paper_2007_10752_b200 as tdes
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    distributed = world > 1
+    if distributed:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if distributed:
+            dist.barrier()
+
+    total_blocks = BLOCKS_PER_GPU * world
+    lo, hi = synthetic.shard_range(total_blocks, world, rank)
+    n = hi - lo
+    sched = tdes.key_schedule(*synthetic.KEYS_3KEY)
+    x = torch.empty(8 * n, dtype=torch.uint8, device=dev)
+    y = torch.empty_like(x)
+    tdes.fill_splitmix64(x, first_index=lo)
+    stream = torch.cuda.current_stream(dev)
+    handle = stream.cuda_stream
+
+    # ---- LOP3 peak microbenchmark (roofline cross-check, same process) ----
+    sms, occ = tdes.device_geometry()
+    sink = torch.empty(sms * 8 * 256, dtype=torch.int32, device=dev)
+    tdes.lop3_peak_launch(sink, sms * 8, 256, 1024)
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    ops = tdes.lop3_peak_launch(sink, sms * 8, 256, 8192)
+    ev1.record(stream)
+    ev1.synchronize()
+    lop3_peak_meas = ops / (ev0.elapsed_time(ev1) * 1e-3) / 1e12   # Tops/s
+
+    # ---- warmup ----
+    for _ in range(args.warmup):
+        tdes.ecb_encrypt_ptr(sched, x.data_ptr(), y.data_ptr(), n, handle)
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps, one fused launch each ----
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    t_begin, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    props = torch.cuda.get_device_properties(dev)
+    bus = None
+    if hasattr(props, "pci_bus_id"):
+        bus = f"{getattr(props, 'pci_domain_id', 0):04x}:{props.pci_bus_id:02x}:{getattr(props, 'pci_device_id', 0):02x}.0"
+    sampler = ClockSampler(bus, local_rank)
+    barrier()
+    torch.cuda.synchronize()
+    with sampler:
+        t_begin.record(stream)
+        for k in range(args.steps):
+            starts[k].record(stream)
+            tdes.ecb_encrypt_ptr(sched, x.data_ptr(), y.data_ptr(), n, handle)
+            ends[k].record(stream)
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    elapsed_ms = t_begin.elapsed_time(t_end)
+    kern_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    if distributed:
+        t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms = float(t.item())
+    clocks = sampler.summary()
+
+    # ---- device-side sanity: decrypt restores the plaintext; digest ----
+    z = torch.empty_like(x)
+    tdes.ecb_decrypt_ptr(sched, y.data_ptr(), z.data_ptr(), n, handle)
+    mismatch = tdes.count_mismatch(z, x)
+    digest = tdes.sum64(y)
+    del z
+    if distributed:
+        t = torch.tensor([mismatch], dtype=torch.int64, device=dev)
+        dist.all_reduce(t)
+        mismatch = int(t.item())
+        d = torch.tensor([digest - (1 << 64) if digest >= (1 << 63) else digest], dtype=torch.int64, device=dev)
+        dist.all_reduce(d)
+        digest = int(d.item()) & ((1 << 64) - 1)
+
+    # ---- e2e: same metric through the host-buffer C-ABI call ----
+    del y
+    torch.cuda.empty_cache()
+    hin = torch.empty(8 * n, dtype=torch.uint8).pin_memory()
+    hin.copy_(x.cpu())
+    del x
+    torch.cuda.empty_cache()
+    hout = torch.empty_like(hin).pin_memory()
+    pipe = tdes.HostPipeline(chunk_blocks=1 << 21, nstreams=4, device=dev)
+    e2e_steps = max(1, min(args.steps, 10))
+    pipe.run(sched, hin, hout)      # warmup
+    torch.cuda.synchronize()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        pipe.run(sched, hin, hout)
+        for s in pipe.streams:
+            stream.wait_stream(s)
+    e1.record(stream)
+    e1.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    if distributed:
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = e2e_steps * total_blocks * 8 / (e2e_ms * 1e-3) / 1e9
+
+    if rank == 0:
+        peaks, peaks_src = read_peaks()
+        info = tdes.kernel_info()
+        T = info.sbox_lop3_total
+        g_alg = 48 * (48 + T + 32) / 32            # ALU ops per block
+        avg_kern_s = sum(kern_ms) / len(kern_ms) * 1e-3
+        achieved = g_alg * n / avg_kern_s / 1e12    # Tops/s on this rank's launches
+        sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+        peak = sms * LOP3_LANES_PER_SM * sm_max * 1e6 / 1e12
+        tb, tsrc = read_traffic()
+        value = args.steps * total_blocks * 8 / (elapsed_ms * 1e-3) / 1e9
+        hbm_gbs = 16 * n / avg_kern_s / 1e9
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "blocks_per_gpu": BLOCKS_PER_GPU,
+                       "bytes_per_gpu": BLOCKS_PER_GPU * 8, "total_blocks": total_blocks,
+                       "op": "encrypt", "keys": "3-key", "parallelism": f"dp{world} (block-range shards)",
+                       "l2": "inputs and outputs 1 GiB per GPU > 126 MB L2; no flush needed",
+                       "Gblocks_per_s": value / 8},
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tops/s",
+                         "frac": achieved / peak,
+                         "traffic": (tb * n if tb is not None else None),
+                         "ops_per_block": g_alg, "sbox_lop3_total": T,
+                         "peak_basis": f"{sms} SMs x {LOP3_LANES_PER_SM} LOP3 lanes/clk x {sm_max:.0f} MHz (sm_max_mhz, {peaks_src})",
+                         "peak_microbench": lop3_peak_meas,
+                         "frac_of_microbench": achieved / lop3_peak_meas,
+                         "kernel_ms_avg": avg_kern_s * 1e3,
+                         "hbm": {"achieved_gbs": hbm_gbs, "peak_gbs": float(peaks.get("hbm_gbs", HBM_PEAK_FALLBACK)),
+                                 "frac": hbm_gbs / float(peaks.get("hbm_gbs", HBM_PEAK_FALLBACK)),
+                                 "bytes_per_block": 16, "peak_source": peaks_src},
+                         "traffic_source": tsrc},
+            "clocks": clocks,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * n,
+                    "d2h_bytes_per_step": 8 * n,
+                    "how": "tdes_ecb_crypt_host: pinned host in/out, 32 MiB chunks on 4 streams (H2D, kernel, D2H overlapped)",
+                    "steps": e2e_steps},
+            "gpu_launches": args.steps,
+            "check": {"device_roundtrip_mismatch_blocks": mismatch, "ciphertext_sum64": f"{digest:016x}"},
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            v, used, sample, secs = oracle_rate(args.cpu_seconds, 1 << 22)
+            line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": used, "kind": "oracle",
+                                    "sample": sample, "seconds": secs, "host_cores": host_cores()}
+        print(json.dumps(line), flush=True)
+    if distributed:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    rank = env_int("RANK", 0)
+    world = env_int("WORLD_SIZE", 1)
+    local_rank = env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    return run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

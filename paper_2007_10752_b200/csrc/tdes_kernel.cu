@@ -28,17 +28,20 @@
 
 namespace {
 
-constexpr int kThreads = 256;        // 8 warps per CTA
-constexpr int kMinCtasPerSm = 2;     // => <= 128 registers per thread
+constexpr int kThreads = 512;        // 16 warps per CTA, one CTA per SM
+constexpr int kMinCtasPerSm = 1;     // => <= 128 registers per thread (64K-register file)
 constexpr int kBlocksPerThread = 32; // one bit-plane word
 constexpr int kTileBlocks = 32 * kBlocksPerThread;  // per warp: 1024 blocks = 8 KiB
-constexpr int kWarpsPerCta = kThreads / 32;
 
 thread_local int g_last_cuda_error = 0;
 
+// Launch-parameter key material, consumption order (round, E-bit):
+//   k = all-ones / all-zeros lane mask of the subkey bit, s = k | 1 (+1 or -1),
+// so that the key XOR runs as one IMAD x * s + k (tdes_gen::kxor).
 template <int NROUNDS>
 struct RoundMasks {
-  uint32_t m[NROUNDS][48];  // all-ones / all-zeros per key bit, consumption order
+  uint32_t s[NROUNDS][48];
+  uint32_t k[NROUNDS][48];
 };
 
 // In-register 32x32 bit-matrix transpose: a[i] bit j <-> a[j] bit i.
@@ -71,113 +74,119 @@ __device__ __forceinline__ void transpose32(uint32_t (&a)[32]) {
   }
 }
 
-// One DES stage as 16 rounds starting with the given half (A = IP left half).
-template <bool START_A, int NR>
-__device__ __forceinline__ void des_stage(uint32_t (&P)[64], const RoundMasks<NR>& mk, int r0) {
+// One warp tile: 32 lanes x 32 blocks = 1024 consecutive blocks from `base`.
+// VEC4: in/out 16-byte aligned -> 128-bit accesses (2 blocks per access).
+template <int NSTAGES, bool VEC4>
+__device__ __forceinline__ void crypt_tile(const uint2* in, uint2* out, size_t base, size_t nblocks,
+                                           unsigned lane, const RoundMasks<16 * NSTAGES>& mk) {
+  const bool full = base + kTileBlocks <= nblocks;
+  uint32_t X[32], Y[32];
+  // ---- S1: load.  Plane bit i <-> the i-th block this lane loads. ----
+  if (VEC4) {
+    const uint4* in4 = reinterpret_cast<const uint4*>(in + base);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const size_t b = base + 64 * i + 2 * lane;
+      uint4 v;
+      if (full || b + 1 < nblocks) {
+        v = __ldcs(in4 + 32 * i + lane);
+      } else {
+        v = make_uint4(0u, 0u, 0u, 0u);
+        if (b < nblocks) {
+          const uint2 h = __ldcs(in + b);
+          v.x = h.x;
+          v.y = h.y;
+        }
+      }
+      X[2 * i] = v.x;
+      Y[2 * i] = v.y;
+      X[2 * i + 1] = v.z;
+      Y[2 * i + 1] = v.w;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const size_t b = base + 32 * i + lane;
+      uint2 v = make_uint2(0u, 0u);
+      if (full || b < nblocks) v = __ldcs(in + b);
+      X[i] = v.x;
+      Y[i] = v.y;
+    }
+  }
+  // ---- S2: to bit-planes ----
+  transpose32(X);
+  transpose32(Y);
+  uint32_t P[64];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    P[j] = X[j];
+    P[32 + j] = Y[j];
+  }
+  // ---- S3..S6: IP (renaming), 16*NSTAGES rounds, FP (renaming) ----
+  // One two-round loop body for all stages keeps the 16 warps of the SM inside
+  // the instruction cache.  The middle stage starts on the half the first one
+  // updated last, so at each stage boundary the halves swap
+  // register roles and the same A-then-B body continues.
 #pragma unroll 1
-  for (int r = r0; r < r0 + 16; r += 2) {
-    if (START_A) {
-      tdes_gen::round_A(P, mk.m[r]);
-      tdes_gen::round_B(P, mk.m[r + 1]);
-    } else {
-      tdes_gen::round_B(P, mk.m[r]);
-      tdes_gen::round_A(P, mk.m[r + 1]);
+  for (int r = 0; r < 16 * NSTAGES; r += 2) {
+    if (NSTAGES == 3 && (r == 16 || r == 32)) tdes_gen::swap_halves(P);
+    tdes_gen::round_A(P, mk.s[r], mk.k[r]);
+    tdes_gen::round_B(P, mk.s[r + 1], mk.k[r + 1]);
+  }
+  uint32_t Q[64];
+  tdes_gen::output_planes(P, Q);
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    X[j] = Q[j];
+    Y[j] = Q[32 + j];
+  }
+  // ---- S7: back to blocks, store ----
+  transpose32(X);
+  transpose32(Y);
+  if (VEC4) {
+    uint4* out4 = reinterpret_cast<uint4*>(out + base);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const size_t b = base + 64 * i + 2 * lane;
+      const uint4 v = make_uint4(X[2 * i], Y[2 * i], X[2 * i + 1], Y[2 * i + 1]);
+      if (full || b + 1 < nblocks) {
+        __stcs(out4 + 32 * i + lane, v);
+      } else if (b < nblocks) {
+        __stcs(out + b, make_uint2(v.x, v.y));
+      }
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const size_t b = base + 32 * i + lane;
+      if (full || b < nblocks) __stcs(out + b, make_uint2(X[i], Y[i]));
     }
   }
 }
 
 // NSTAGES = 3: fused 3DES (48 rounds); NSTAGES = 1: single DES (16 rounds).
-// VEC4: in/out 16-byte aligned -> 128-bit accesses (2 blocks per access).
+// Work distribution: CTA c owns the contiguous tile range
+// [ntiles*c/grid, ntiles*(c+1)/grid); its 16 warps claim tiles one at a time
+// from a shared-memory counter.  Warps of one SM progress at very different
+// rates under the hardware's warp arbitration, so a static per-warp split
+// leaves the SM waiting on its slowest warp (measured: 1.6-2x slower).
 template <int NSTAGES, bool VEC4>
 __global__ void __launch_bounds__(kThreads, kMinCtasPerSm)
 tdes_ecb_kernel(const uint2* in, uint2* out, size_t nblocks,
                 const __grid_constant__ RoundMasks<16 * NSTAGES> mk) {
+  __shared__ unsigned int next_tile;
   const unsigned lane = threadIdx.x & 31u;
   const size_t ntiles = (nblocks + kTileBlocks - 1) / kTileBlocks;
-  const size_t nwarps = ((size_t)gridDim.x * blockDim.x) >> 5;
-  for (size_t tile = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; tile < ntiles;
-       tile += nwarps) {
-    const size_t base = tile * kTileBlocks;
-    const bool full = base + kTileBlocks <= nblocks;
-    uint32_t X[32], Y[32];
-    // ---- S1: load.  Plane bit i <-> the i-th block this lane loads. ----
-    if (VEC4) {
-      const uint4* in4 = reinterpret_cast<const uint4*>(in + base);
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const size_t b = base + 64 * i + 2 * lane;
-        uint4 v;
-        if (full || b + 1 < nblocks) {
-          v = __ldcs(in4 + 32 * i + lane);
-        } else {
-          v = make_uint4(0u, 0u, 0u, 0u);
-          if (b < nblocks) {
-            const uint2 h = __ldcs(in + b);
-            v.x = h.x;
-            v.y = h.y;
-          }
-        }
-        X[2 * i] = v.x;
-        Y[2 * i] = v.y;
-        X[2 * i + 1] = v.z;
-        Y[2 * i + 1] = v.w;
-      }
-    } else {
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const size_t b = base + 32 * i + lane;
-        uint2 v = make_uint2(0u, 0u);
-        if (full || b < nblocks) v = __ldcs(in + b);
-        X[i] = v.x;
-        Y[i] = v.y;
-      }
-    }
-    // ---- S2: to bit-planes ----
-    transpose32(X);
-    transpose32(Y);
-    uint32_t P[64];
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      P[j] = X[j];
-      P[32 + j] = Y[j];
-    }
-    // ---- S3..S6: IP (renaming), 16*NSTAGES rounds, FP (renaming) ----
-    if (NSTAGES == 3) {
-      des_stage<true>(P, mk, 0);    // E_K1      (first round updates A)
-      des_stage<false>(P, mk, 16);  // D_K2      (starts on the half updated last)
-      des_stage<true>(P, mk, 32);   // E_K3
-    } else {
-      des_stage<true>(P, mk, 0);
-    }
-    uint32_t Q[64];
-    tdes_gen::output_planes(P, Q);
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      X[j] = Q[j];
-      Y[j] = Q[32 + j];
-    }
-    // ---- S7: back to blocks, store ----
-    transpose32(X);
-    transpose32(Y);
-    if (VEC4) {
-      uint4* out4 = reinterpret_cast<uint4*>(out + base);
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const size_t b = base + 64 * i + 2 * lane;
-        const uint4 v = make_uint4(X[2 * i], Y[2 * i], X[2 * i + 1], Y[2 * i + 1]);
-        if (full || b + 1 < nblocks) {
-          __stcs(out4 + 32 * i + lane, v);
-        } else if (b < nblocks) {
-          __stcs(out + b, make_uint2(v.x, v.y));
-        }
-      }
-    } else {
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const size_t b = base + 32 * i + lane;
-        if (full || b < nblocks) __stcs(out + b, make_uint2(X[i], Y[i]));
-      }
-    }
+  const size_t lo = ntiles * blockIdx.x / gridDim.x;
+  const size_t hi = ntiles * (blockIdx.x + 1) / gridDim.x;
+  if (threadIdx.x == 0) next_tile = 0;
+  __syncthreads();
+  for (;;) {
+    unsigned t = 0;
+    if (lane == 0) t = atomicAdd(&next_tile, 1u);
+    const size_t tile = lo + __shfl_sync(0xffffffffu, t, 0);
+    if (tile >= hi) break;
+    crypt_tile<NSTAGES, VEC4>(in, out, tile * kTileBlocks, nblocks, lane, mk);
   }
 }
 
@@ -231,17 +240,22 @@ int launch(const uint32_t (*masks)[48], const void* in, void* out, size_t nblock
   if (rc) return rc;
   if (nblocks > (SIZE_MAX >> 4)) return TDES_ERR_INVALID_ARG;
   RoundMasks<16 * NSTAGES> mk;
-  memcpy(mk.m, masks, sizeof mk.m);
+  for (int r = 0; r < 16 * NSTAGES; ++r)
+    for (int b = 0; b < 48; ++b) {
+      const uint32_t m = masks[r][b] ? 0xFFFFFFFFu : 0u;
+      mk.k[r][b] = m;
+      mk.s[r][b] = m | 1u;
+    }
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return cuda_fail(e);
   if (dev < 0 || dev >= kMaxDevices) return TDES_ERR_INVALID_ARG;
   const bool vec4 = (((uintptr_t)in | (uintptr_t)out) & 15u) == 0;
   const size_t ntiles = (nblocks + kTileBlocks - 1) / kTileBlocks;
-  const size_t want = (ntiles + kWarpsPerCta - 1) / kWarpsPerCta;
+  // one resident CTA per SM; with fewer tiles than SMs, one tile per CTA
   const int occ = vec4 ? occupancy<NSTAGES, true>(dev) : occupancy<NSTAGES, false>(dev);
   const size_t resident = (size_t)num_sms(dev) * (size_t)occ;
-  const unsigned grid = (unsigned)(want < resident ? want : resident);
+  const unsigned grid = (unsigned)(ntiles < resident ? ntiles : resident);
   const uint2* pin = static_cast<const uint2*>(in);
   uint2* pout = static_cast<uint2*>(out);
   if (vec4)

@@ -76,8 +76,10 @@ def emulate(man, circs, blocks_u8, masks):
             sig = list(xs)
             for lut, a, b, c in circs[g]["gates"]:
                 sig.append(lut_np(lut, sig[a], sig[b], sig[c]))
+            neg = circs[g].get("neg") or [0, 0, 0, 0]
             for o in range(4):
-                upd[dst[pinv[4 * g + o]]] = sig[circs[g]["outputs"][o]]
+                v = sig[circs[g]["outputs"][o]]
+                upd[dst[pinv[4 * g + o]]] = ~v if neg[o] else v
         for d, v in upd.items():
             P[d] = P[d] ^ v
     Q = [P[man["out_src"][k]] for k in range(64)]

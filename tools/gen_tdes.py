@@ -76,7 +76,8 @@ def eval_circuit(circ, inputs=None, full=FULL):
     sig = list(inputs if inputs is not None else VARS)
     for lut, a, b, c in circ["gates"]:
         sig.append(lut_eval(lut, sig[a], sig[b], sig[c], full))
-    return [sig[s] for s in circ["outputs"]]
+    neg = circ.get("neg") or [0, 0, 0, 0]
+    return [sig[s] ^ (full if n else 0) for s, n in zip(circ["outputs"], neg)]
 
 
 def verify_circuit(g: int, circ) -> bool:
@@ -131,7 +132,7 @@ def load_searched():
         for item in data.get("circuits", []):
             g = item["sbox"]
             circ = {"gates": item["gates"], "outputs": item["outputs"],
-                    "source": os.path.basename(path)}
+                    "neg": item.get("neg", [0, 0, 0, 0]), "source": os.path.basename(path)}
             if not verify_circuit(g, circ):
                 print(f"warning: {path} S{g + 1} circuit fails verification; ignored", file=sys.stderr)
                 continue
@@ -208,8 +209,10 @@ def emit_sbox(g, circ):
         return f"x{s}" if s < 6 else f"t{s - 6}"
     for k, (lut, a, b, c) in enumerate(circ["gates"]):
         lines.append(f"  const uint32_t t{k} = lop3<0x{lut:02x}>({name(a)}, {name(b)}, {name(c)});")
+    neg = circ.get("neg") or [0, 0, 0, 0]
     for o, s in enumerate(circ["outputs"]):
-        lines.append(f"  o{o} = {name(s)};")
+        # a complemented output costs nothing: the Feistel XOR becomes an XNOR (one LOP3)
+        lines.append(f"  o{o} = {'~' if neg[o] else ''}{name(s)};")
     lines.append("}")
     return "\n".join(lines)
 
@@ -221,10 +224,12 @@ def emit_round(half):
     for i, m in enumerate(P_SRC):
         pinv[m] = i
     lines = [f"// One Feistel round updating half {half}: {half} ^= P(S(E(other) ^ K)).",
-             f"__device__ __forceinline__ void round_{half}(uint32_t (&P)[64], const uint32_t* __restrict__ K) {{"]
+             "// Key XOR on the FMA pipe: with k in {0, ~0} and s = k | 1, x ^ k == x * s + k.",
+             f"__device__ __forceinline__ void round_{half}(uint32_t (&P)[64], const uint32_t* __restrict__ S,",
+             "                                        const uint32_t* __restrict__ K) {"]
     for g in range(8):
-        xs = [f"P[{src[T.E[6 * g + i] - 1]}] ^ K[{6 * g + i}]" for i in range(6)]
-        lines.append(f"  {{ uint32_t o0, o1, o2, o3;")
+        xs = [f"kxor(P[{src[T.E[6 * g + i] - 1]}], S[{6 * g + i}], K[{6 * g + i}])" for i in range(6)]
+        lines.append("  { uint32_t o0, o1, o2, o3;")
         lines.append(f"    sbox{g + 1}({', '.join(xs)}, o0, o1, o2, o3);")
         for o in range(4):
             lines.append(f"    P[{dst[pinv[4 * g + o]]}] ^= o{o};")
@@ -241,14 +246,24 @@ def emit_header(circs):
         "// Bitsliced DES building blocks for the sm_100a 3DES-ECB kernel.",
         "// Planes: P[32*w + j] holds bit j of little-endian word w of each of the",
         "// thread's 32 blocks (bit i of a plane = block i).",
-        f"// S-box LOP3 total T = {total} per round; per round ops = 48 key XOR + T + 32 Feistel XOR.",
+        f"// S-box LOP3 total T = {total} per round; per round: 48 key-XOR IMAD (FMA pipe) + T + 32 Feistel-XOR LOP3 (ALU pipe).",
         "#pragma once",
         "#include <stdint.h>",
         "",
         "namespace tdes_gen {",
         "",
         f"constexpr int kSboxLop3Total = {total};",
+
         f"constexpr int kSboxLop3[8] = {{{', '.join(str(len(c['gates'])) for c in circs)}}};",
+        "",
+        "// x ^ k for a lane mask k in {0, 0xFFFFFFFF}, given s = k | 1 (= +1 or -1):",
+        "// x * s + k is x (k = 0) or -x - 1 = ~x (k = ~0).  One IMAD on the FMA pipe,",
+        "// leaving the integer ALU pipe (the kernel's bound) to the S-box LOP3s.",
+        "__device__ __forceinline__ uint32_t kxor(uint32_t x, uint32_t s, uint32_t k) {",
+        "  uint32_t d;",
+        "  asm(\"mad.lo.u32 %0, %1, %2, %3;\" : \"=r\"(d) : \"r\"(x), \"r\"(s), \"r\"(k));",
+        "  return d;",
+        "}",
         "",
         "template <unsigned LUT>",
         "__device__ __forceinline__ uint32_t lop3(uint32_t a, uint32_t b, uint32_t c) {",
@@ -264,6 +279,12 @@ def emit_header(circs):
     h.append(emit_round("A"))
     h.append("")
     h.append(emit_round("B"))
+    h.append("")
+    h.append("// Exchange the register roles of the halves A (IP left, L0) and B (IP right, R0).")
+    h.append("__device__ __forceinline__ void swap_halves(uint32_t (&P)[64]) {")
+    for a, b in zip(A_IDX, B_IDX):
+        h.append(f"  {{ const uint32_t t = P[{a}]; P[{a}] = P[{b}]; P[{b}] = t; }}")
+    h.append("}")
     h.append("")
     h.append("// Pre-output (B || A) through FP, renamed into store-transpose order (PAPER.md:74-75).")
     h.append("__device__ __forceinline__ void output_planes(const uint32_t (&P)[64], uint32_t (&Q)[64]) {")
@@ -298,7 +319,8 @@ def manifest(circs):
         "sbox_lop3": [len(c["gates"]) for c in circs],
         "sbox_lop3_total": sum(len(c["gates"]) for c in circs),
         "sources": [c["source"] for c in circs],
-        "circuits": [{"sbox": g, "gates": c["gates"], "outputs": c["outputs"]} for g, c in enumerate(circs)],
+        "circuits": [{"sbox": g, "gates": c["gates"], "outputs": c["outputs"],
+                      "neg": c.get("neg") or [0, 0, 0, 0]} for g, c in enumerate(circs)],
         "a_idx": A_IDX, "b_idx": B_IDX, "p_src": P_SRC, "out_src": OUT_SRC,
         "round_schedule": round_schedule(),
     }

@@ -1,0 +1,292 @@
+/*
+ * sbox_search.c -- search for small 3-input-LUT (LOP3) circuits computing the
+ * four output bits of one DES S-box (6 inputs -> 4 outputs).
+ *
+ * Method: recursive Shannon-style decomposition in the spirit of Kwan,
+ * "Reducing the Gate Count of Bitslice DES" (2000), adapted to arbitrary
+ * 3-input gates:
+ *   create(target, mask):
+ *     1. an existing signal equals target (or its complement) on mask -> reuse;
+ *     2. one new LUT over any three existing signals fits target on mask;
+ *     3. otherwise pick a selector input x_i not yet used on this path, build
+ *        f0 for the x_i = 0 half, then f1 for the x_i = 1 half either as the
+ *        plain target (mux form) or as target ^ f0 (xor form), and join them
+ *        with one LUT(x_i, f0, f1).  Every selector/form is tried on a copy of
+ *        the circuit at the top `full_levels` levels and the smallest wins;
+ *        deeper levels pick one at random.
+ *   Outputs are built one after another so later ones reuse earlier gates.
+ * Complements are free: a LUT consumer absorbs them, and the kernel XORs each
+ * output into the other Feistel half with XOR or XNOR (one LOP3 either way).
+ *
+ * Many randomized trials (output order, selector order, triple scan order)
+ * run in parallel (OpenMP); the smallest circuit is printed as one JSON line:
+ *   {"gates": [[lut, a, b, c], ...], "outputs": [s0..s3], "neg": [0/1 x4]}
+ * Signals 0..5 are inputs x0..x5 (x0 = S-box input bit b1 = MSB of the 6-bit
+ * value, truth-table bit v has x_i = bit (5-i) of v); signal 6+k is gate k.
+ *
+ * Usage: sbox_search <trials> <seed> <full_levels> <t0> <t1> <t2> <t3>
+ *        (t_o = 64-bit truth table of output bit o, hex)
+ * The result is verified exhaustively by the caller (tools/run_sbox_search.py)
+ * and again by tools/gen_tdes.py before any code is emitted.
+ */
+#include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define MAXG 160
+typedef uint64_t tt_t;
+
+typedef struct {
+  tt_t tt[MAXG];
+  uint8_t lut[MAXG];
+  uint8_t in[MAXG][3];
+  int n;
+} St;
+
+static tt_t VARS[6];
+
+static inline uint64_t rnd(uint64_t *s) {
+  uint64_t z = (*s += 0x9E3779B97F4A7C15ull);
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+static inline tt_t lut_eval(int lut, tt_t a, tt_t b, tt_t c) {
+  tt_t r = 0;
+  for (int k = 0; k < 8; k++)
+    if ((lut >> k) & 1) r |= ((k & 4) ? a : ~a) & ((k & 2) ? b : ~b) & ((k & 1) ? c : ~c);
+  return r;
+}
+
+/* LUT over (A,B,C) equal to T on M, or -1. Unconstrained entries are 0. */
+static inline int fit3(tt_t A, tt_t B, tt_t C, tt_t T, tt_t M) {
+  int lut = 0;
+  const tt_t nA = ~A, nB = ~B, nC = ~C;
+  const tt_t ab[4] = {M & nA & nB, M & nA & B, M & A & nB, M & A & B};
+  for (int q = 0; q < 4; q++) {
+    const tt_t r0 = ab[q] & nC, r1 = ab[q] & C;
+    const tt_t t0 = T & r0, t1 = T & r1;
+    if (t0 && t0 != r0) return -1;
+    if (t1 && t1 != r1) return -1;
+    if (t0) lut |= 1 << (2 * q);
+    if (t1) lut |= 1 << (2 * q + 1);
+  }
+  return lut;
+}
+
+static int add_gate(St *s, int lut, int a, int b, int c) {
+  if (s->n >= MAXG) return -1;
+  const int k = s->n++;
+  s->lut[k] = (uint8_t)lut;
+  s->in[k][0] = (uint8_t)a;
+  s->in[k][1] = (uint8_t)b;
+  s->in[k][2] = (uint8_t)c;
+  s->tt[k] = lut_eval(lut, s->tt[a], s->tt[b], s->tt[c]);
+  return k;
+}
+
+static int find_existing(const St *s, tt_t T, tt_t M, int *neg) {
+  for (int g = s->n - 1; g >= 0; g--) {
+    const tt_t d = (s->tt[g] ^ T) & M;
+    if (!d) { *neg = 0; return g; }
+    if (d == M) { *neg = 1; return g; }
+  }
+  return -1;
+}
+
+/* one new gate over three existing signals (each unordered triple once, keyed
+ * by its smallest index; the outer scan starts at a random index) */
+static int find_single(St *s, tt_t T, tt_t M, uint64_t *rng) {
+  const int n = s->n;
+  const int off = n ? (int)(rnd(rng) % (uint64_t)n) : 0;
+  for (int ia = 0; ia < n; ia++) {
+    const int a = (ia + off) % n;
+    const tt_t A = s->tt[a];
+    for (int b = a + 1; b < n; b++) {
+      const tt_t B = s->tt[b];
+      for (int c = b + 1; c < n; c++) {
+        const int lut = fit3(A, B, s->tt[c], T, M);
+        if (lut >= 0) return add_gate(s, lut, a, b, c);
+      }
+    }
+  }
+  return -1;
+}
+
+typedef struct {
+  int full_levels;
+} Cfg;
+
+static int create(St *s, tt_t T, tt_t M, int selused, int level, const Cfg *cfg, uint64_t *rng,
+                  int *neg);
+
+/* build with selector i in form f (0 mux, 1 xor) on state s; returns signal or -1 */
+static int try_sel(St *s, tt_t T, tt_t M, int selused, int level, int i, int form, const Cfg *cfg,
+                   uint64_t *rng, int *neg) {
+  const tt_t X = VARS[i];
+  int n0, n1;
+  const int f0 = create(s, T, M & ~X, selused | (1 << i), level + 1, cfg, rng, &n0);
+  if (f0 < 0) return -1;
+  const tt_t T1 = form ? (T ^ s->tt[f0]) : T;
+  const int f1 = create(s, T1, M & X, selused | (1 << i), level + 1, cfg, rng, &n1);
+  if (f1 < 0) return -1;
+  /* join: LUT(x_i, f0, f1) = T on M (exists for both forms) */
+  int ex = find_existing(s, T, M, neg);
+  if (ex >= 0) return ex;
+  const int lut = fit3(X, s->tt[f0], s->tt[f1], T, M);
+  if (lut < 0) return -1;
+  *neg = 0;
+  return add_gate(s, lut, i, f0, f1);
+}
+
+static int create(St *s, tt_t T, tt_t M, int selused, int level, const Cfg *cfg, uint64_t *rng,
+                  int *neg) {
+  int g = find_existing(s, T, M, neg);
+  if (g >= 0) return g;
+  g = find_single(s, T, M, rng);
+  if (g >= 0) {
+    *neg = 0;
+    return g;
+  }
+  int cand[6], nc = 0;
+  for (int i = 0; i < 6; i++)
+    if (!(selused & (1 << i))) cand[nc++] = i;
+  if (!nc) return -1;
+  for (int k = nc - 1; k > 0; k--) { /* shuffle */
+    const int j = (int)(rnd(rng) % (uint64_t)(k + 1));
+    const int t = cand[k];
+    cand[k] = cand[j];
+    cand[j] = t;
+  }
+  if (level >= cfg->full_levels) {
+    const int form = (int)(rnd(rng) & 1);
+    return try_sel(s, T, M, selused, level, cand[0], form, cfg, rng, neg);
+  }
+  St *best = NULL, *tmp = (St *)malloc(sizeof(St));
+  int bestg = -1, bestneg = 0;
+  for (int k = 0; k < nc; k++) {
+    for (int form = 0; form < 2; form++) {
+      memcpy(tmp, s, sizeof(St));
+      int ng;
+      const int r = try_sel(tmp, T, M, selused, level, cand[k], form, cfg, rng, &ng);
+      if (r < 0) continue;
+      if (!best || tmp->n < best->n) {
+        if (!best) best = (St *)malloc(sizeof(St));
+        memcpy(best, tmp, sizeof(St));
+        bestg = r;
+        bestneg = ng;
+      }
+    }
+  }
+  free(tmp);
+  if (!best) return -1;
+  memcpy(s, best, sizeof(St));
+  free(best);
+  *neg = bestneg;
+  return bestg;
+}
+
+typedef struct {
+  St s;
+  int out[4], neg[4];
+} Result;
+
+static void run_trial(const tt_t targets[4], const Cfg *cfg, uint64_t seed, Result *res) {
+  uint64_t rng = seed;
+  St *s = &res->s;
+  memset(s, 0, sizeof *s);
+  for (int i = 0; i < 6; i++) s->tt[i] = VARS[i];
+  s->n = 6;
+  int order[4] = {0, 1, 2, 3};
+  for (int k = 3; k > 0; k--) {
+    const int j = (int)(rnd(&rng) % (uint64_t)(k + 1));
+    const int t = order[k];
+    order[k] = order[j];
+    order[j] = t;
+  }
+  for (int q = 0; q < 4; q++) {
+    const int o = order[q];
+    int ng = 0;
+    const int g = create(s, targets[o], ~0ull, 0, 0, cfg, &rng, &ng);
+    if (g < 0) {
+      s->n = MAXG + 1;
+      return;
+    }
+    res->out[o] = g;
+    res->neg[o] = ng;
+  }
+}
+
+/* remove gates not reachable from the outputs, renumber */
+static void prune(Result *r) {
+  St *s = &r->s;
+  int live[MAXG] = {0};
+  for (int o = 0; o < 4; o++) live[r->out[o]] = 1;
+  for (int g = s->n - 1; g >= 6; g--)
+    if (live[g])
+      for (int j = 0; j < 3; j++) live[s->in[g][j]] = 1;
+  int map[MAXG];
+  St t;
+  memset(&t, 0, sizeof t);
+  for (int i = 0; i < 6; i++) {
+    t.tt[i] = s->tt[i];
+    map[i] = i;
+  }
+  t.n = 6;
+  for (int g = 6; g < s->n; g++) {
+    if (!live[g]) continue;
+    map[g] = add_gate(&t, s->lut[g], map[s->in[g][0]], map[s->in[g][1]], map[s->in[g][2]]);
+  }
+  for (int o = 0; o < 4; o++) r->out[o] = map[r->out[o]];
+  memcpy(s, &t, sizeof t);
+}
+
+int main(int argc, char **argv) {
+  if (argc != 8) {
+    fprintf(stderr, "usage: %s trials seed full_levels t0 t1 t2 t3\n", argv[0]);
+    return 2;
+  }
+  const long trials = atol(argv[1]);
+  const uint64_t seed = strtoull(argv[2], 0, 10);
+  Cfg cfg = {atoi(argv[3])};
+  tt_t targets[4];
+  for (int o = 0; o < 4; o++) targets[o] = strtoull(argv[4 + o], 0, 16);
+  for (int i = 0; i < 6; i++) {
+    VARS[i] = 0;
+    for (int v = 0; v < 64; v++)
+      if ((v >> (5 - i)) & 1) VARS[i] |= 1ull << v;
+  }
+  Result best;
+  best.s.n = MAXG + 1;
+#pragma omp parallel
+  {
+    Result *r = (Result *)malloc(sizeof(Result));
+#pragma omp for schedule(dynamic, 1)
+    for (long t = 0; t < trials; t++) {
+      run_trial(targets, &cfg, seed * 1000003ull + (uint64_t)t * 7919ull + 1, r);
+      if (r->s.n > MAXG) continue;
+      prune(r);
+#pragma omp critical
+      {
+        if (r->s.n < best.s.n) memcpy(&best, r, sizeof(Result));
+      }
+    }
+    free(r);
+  }
+  if (best.s.n > MAXG) {
+    printf("{\"error\": \"no circuit\"}\n");
+    return 1;
+  }
+  printf("{\"gates\": [");
+  for (int g = 6; g < best.s.n; g++)
+    printf("%s[%d, %d, %d, %d]", g > 6 ? ", " : "", best.s.lut[g], best.s.in[g][0], best.s.in[g][1],
+           best.s.in[g][2]);
+  printf("], \"outputs\": [%d, %d, %d, %d], \"neg\": [%d, %d, %d, %d]}\n", best.out[0], best.out[1],
+         best.out[2], best.out[3], best.neg[0], best.neg[1], best.neg[2], best.neg[3]);
+  return 0;
+}
