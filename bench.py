@@ -235,8 +235,9 @@ def run_ours(args, rank, world, local_rank):
         if distributed:
             dist.barrier()
 
+    from paper_2007_10752_b200 import shard
     total_blocks = BLOCKS_PER_GPU * world
-    lo, hi = synthetic.shard_range(total_blocks, world, rank)
+    lo, hi = shard.shard_range(total_blocks, world, rank)
     n = hi - lo
     sched = tdes.key_schedule(*synthetic.KEYS_3KEY)
     x = torch.empty(8 * n, dtype=torch.uint8, device=dev)
@@ -284,10 +285,7 @@ def run_ours(args, rank, world, local_rank):
     barrier()
     elapsed_ms = t_begin.elapsed_time(t_end)
     kern_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    if distributed:
-        t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed_ms = float(t.item())
+    elapsed_ms = shard.max_over_ranks(elapsed_ms)
     clocks = sampler.summary()
 
     # ---- device-side sanity: decrypt restores the plaintext; digest ----
@@ -296,13 +294,8 @@ def run_ours(args, rank, world, local_rank):
     mismatch = tdes.count_mismatch(z, x)
     digest = tdes.sum64(y)
     del z
-    if distributed:
-        t = torch.tensor([mismatch], dtype=torch.int64, device=dev)
-        dist.all_reduce(t)
-        mismatch = int(t.item())
-        d = torch.tensor([digest - (1 << 64) if digest >= (1 << 63) else digest], dtype=torch.int64, device=dev)
-        dist.all_reduce(d)
-        digest = int(d.item()) & ((1 << 64) - 1)
+    mismatch = shard.sum_over_ranks(mismatch)
+    digest = shard.sum_u64_over_ranks(digest)
 
     # ---- e2e: same metric through the host-buffer C-ABI call ----
     del y
@@ -326,10 +319,7 @@ def run_ours(args, rank, world, local_rank):
     e1.record(stream)
     e1.synchronize()
     e2e_ms = e0.elapsed_time(e1)
-    if distributed:
-        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+    e2e_ms = shard.max_over_ranks(e2e_ms)
     e2e_value = e2e_steps * total_blocks * 8 / (e2e_ms * 1e-3) / 1e9
 
     if rank == 0:

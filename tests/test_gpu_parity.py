@@ -225,3 +225,22 @@ def test_config1_full_vs_oracle(tdes):
 def test_ragged_large_size(tdes):
     # not a multiple of the 1024-block warp tile, and more tiles than resident warps
     _sampled_check(tdes, synthetic.KEYS_3KEY, (1 << 23) + 777, nsample=4096)
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_shard_invariance_on_device(tdes, world):
+    """Encrypting each rank's block range separately == one launch over everything (§8e)."""
+    from paper_2007_10752_b200 import shard
+    n = (1 << 20) + 13
+    s = tdes.key_schedule(*synthetic.KEYS_3KEY)
+    x = torch.empty(8 * n, dtype=torch.uint8, device="cuda")
+    tdes.fill_splitmix64(x)
+    whole = tdes.ecb_encrypt(x, s)
+    parts = torch.empty_like(x)
+    for r in range(world):
+        lo, hi = shard.shard_range(n, world, r)
+        xr = torch.empty(8 * (hi - lo), dtype=torch.uint8, device="cuda")
+        tdes.fill_splitmix64(xr, first_index=lo)           # each rank generates its own shard
+        parts[8 * lo:8 * hi] = tdes.ecb_encrypt(xr, s)
+    assert torch.equal(parts, whole)
+    assert tdes.sum64(parts) == tdes.sum64(whole)

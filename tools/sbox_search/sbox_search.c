@@ -24,7 +24,8 @@
  * Signals 0..5 are inputs x0..x5 (x0 = S-box input bit b1 = MSB of the 6-bit
  * value, truth-table bit v has x_i = bit (5-i) of v); signal 6+k is gate k.
  *
- * Usage: sbox_search <trials> <seed> <full_levels> <t0> <t1> <t2> <t3>
+ * Usage: sbox_search <trials> <seed> <levels> <t0> <t1> <t2> <t3>
+ *        levels = full_levels + 10 * all_forms (all_forms: try AND/OR join forms too)
  *        (t_o = 64-bit truth table of output bit o, hex)
  * The result is verified exhaustively by the caller (tools/run_sbox_search.py)
  * and again by tools/gen_tdes.py before any code is emitted.
@@ -120,28 +121,52 @@ static int find_single(St *s, tt_t T, tt_t M, uint64_t *rng) {
 
 typedef struct {
   int full_levels;
+  int all_forms;
 } Cfg;
 
 static int create(St *s, tt_t T, tt_t M, int selused, int level, const Cfg *cfg, uint64_t *rng,
                   int *neg);
 
-/* build with selector i in form f (0 mux, 1 xor) on state s; returns signal or -1 */
-static int try_sel(St *s, tt_t T, tt_t M, int selused, int level, int i, int form, const Cfg *cfg,
-                   uint64_t *rng, int *neg) {
-  const tt_t X = VARS[i];
+/* Build T on M with selector input i.  The half x_i = `first` is built first
+ * (f0), then the other half (f1) with the join form `form`:
+ *   0 mux      f1 = T
+ *   1 xor      f1 = T ^ f0
+ *   2 and      T = f0 & f1 on the other half (needs T => f0 there): f1 free where f0 = 0
+ *   3 andn     T = ~f0 & f1 (needs T => ~f0): f1 free where f0 = 1
+ *   4 or       T = f0 | f1 (needs f0 => T): f1 free where f0 = 1
+ *   5 orn      T = ~f0 | f1 (needs ~f0 => T): f1 free where f0 = 0
+ * and one LUT(x_i, f0, f1) joins them (fit3 finds it for every polarity).
+ * Returns the signal or -1 (also when the form's precondition fails). */
+#define NFORMS 6
+static int try_sel(St *s, tt_t T, tt_t M, int selused, int level, int i, int first, int form,
+                   const Cfg *cfg, uint64_t *rng, int *neg) {
+  const tt_t X = first ? VARS[i] : ~VARS[i];   /* region built first */
+  const tt_t M0 = M & X, M1 = M & ~X;
   int n0, n1;
-  const int f0 = create(s, T, M & ~X, selused | (1 << i), level + 1, cfg, rng, &n0);
+  const int f0 = create(s, T, M0, selused | (1 << i), level + 1, cfg, rng, &n0);
   if (f0 < 0) return -1;
-  const tt_t T1 = form ? (T ^ s->tt[f0]) : T;
-  const int f1 = create(s, T1, M & X, selused | (1 << i), level + 1, cfg, rng, &n1);
-  if (f1 < 0) return -1;
-  /* join: LUT(x_i, f0, f1) = T on M (exists for both forms) */
+  const tt_t F = s->tt[f0];
+  tt_t T1 = T, K1 = M1;
+  switch (form) {
+    case 0: break;
+    case 1: T1 = T ^ F; break;
+    case 2: if (T & ~F & M1) return -1; K1 = M1 & F; break;
+    case 3: if (T & F & M1) return -1; K1 = M1 & ~F; break;
+    case 4: if (~T & F & M1) return -1; K1 = M1 & ~F; break;
+    case 5: if (~T & ~F & M1) return -1; K1 = M1 & F; break;
+  }
+  int f1 = -1;
+  if (K1) {
+    f1 = create(s, T1, K1, selused | (1 << i), level + 1, cfg, rng, &n1);
+    if (f1 < 0) return -1;
+  }
   int ex = find_existing(s, T, M, neg);
   if (ex >= 0) return ex;
-  const int lut = fit3(X, s->tt[f0], s->tt[f1], T, M);
+  const int g1 = f1 >= 0 ? f1 : f0;
+  const int lut = fit3(VARS[i], F, s->tt[g1], T, M);
   if (lut < 0) return -1;
   *neg = 0;
-  return add_gate(s, lut, i, f0, f1);
+  return add_gate(s, lut, i, f0, g1);
 }
 
 static int create(St *s, tt_t T, tt_t M, int selused, int level, const Cfg *cfg, uint64_t *rng,
@@ -164,16 +189,28 @@ static int create(St *s, tt_t T, tt_t M, int selused, int level, const Cfg *cfg,
     cand[j] = t;
   }
   if (level >= cfg->full_levels) {
-    const int form = (int)(rnd(rng) & 1);
-    return try_sel(s, T, M, selused, level, cand[0], form, cfg, rng, neg);
+    /* greedy below the fully explored levels: random selector, first feasible form */
+    const int first = (int)(rnd(rng) & 1);
+    const int f0form = (int)(rnd(rng) % NFORMS);
+    St *tmp = (St *)malloc(sizeof(St));
+    int r = -1;
+    for (int q = 0; q < NFORMS && r < 0; q++) {
+      memcpy(tmp, s, sizeof(St));
+      r = try_sel(tmp, T, M, selused, level, cand[0], first, (f0form + q) % NFORMS, cfg, rng, neg);
+      if (r >= 0) memcpy(s, tmp, sizeof(St));
+    }
+    free(tmp);
+    return r;
   }
   St *best = NULL, *tmp = (St *)malloc(sizeof(St));
   int bestg = -1, bestneg = 0;
   for (int k = 0; k < nc; k++) {
-    for (int form = 0; form < 2; form++) {
+    for (int fw = 0; fw < 2 * NFORMS; fw++) {
+      const int first = fw / NFORMS, form = fw % NFORMS;
+      if (!cfg->all_forms && form > 1) continue;
       memcpy(tmp, s, sizeof(St));
       int ng;
-      const int r = try_sel(tmp, T, M, selused, level, cand[k], form, cfg, rng, &ng);
+      const int r = try_sel(tmp, T, M, selused, level, cand[k], first, form, cfg, rng, &ng);
       if (r < 0) continue;
       if (!best || tmp->n < best->n) {
         if (!best) best = (St *)malloc(sizeof(St));
@@ -253,7 +290,7 @@ int main(int argc, char **argv) {
   }
   const long trials = atol(argv[1]);
   const uint64_t seed = strtoull(argv[2], 0, 10);
-  Cfg cfg = {atoi(argv[3])};
+  Cfg cfg = {atoi(argv[3]) % 10, atoi(argv[3]) >= 10};
   tt_t targets[4];
   for (int o = 0; o < 4; o++) targets[o] = strtoull(argv[4 + o], 0, 16);
   for (int i = 0; i < 6; i++) {
