@@ -227,7 +227,7 @@ def run_ours(args, rank, world, local_rank):
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    distributed = world > 1
+    distributed = world > 1 or "TORCHELASTIC_RUN_ID" in os.environ  # torchrun: exercise NCCL even at N=1
     if distributed:
         dist.init_process_group("nccl", device_id=dev)
 

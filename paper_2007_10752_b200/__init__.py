@@ -16,7 +16,7 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtdes_b200.so")
+LIB_PATH = os.environ.get("TDES_LIB_PATH") or os.path.join(_HERE, "libtdes_b200.so")  # override: experiments only
 
 TDES_OK = 0
 ERRORS = {-1: "TDES_ERR_INVALID_ARG", -2: "TDES_ERR_MISALIGNED", -3: "TDES_ERR_OVERLAP",
@@ -76,6 +76,7 @@ def _load():
                             ctypes.POINTER(ctypes.c_uint64), vp], ctypes.c_int),
         "tdes_device_geometry": ([ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)],
                                  ctypes.c_int),
+        "tdes_paper_ecb": ([vp, vp, vp, sz, ctypes.c_int, vp, sz, vp], ctypes.c_int),
     }
     for name, (argtypes, restype) in sig.items():
         fn = getattr(lib, name)
@@ -90,7 +91,7 @@ _lib = _load()
 EXPORTS = ("tdes_key_schedule", "tdes_ecb_encrypt", "tdes_ecb_decrypt", "des_key_schedule",
            "des_ecb_encrypt", "des_ecb_decrypt", "tdes_ecb_crypt_host", "tdes_get_kernel_info",
            "tdes_strerror", "tdes_last_cuda_error", "tdes_fill_splitmix64", "tdes_sum64",
-           "tdes_count_mismatch", "tdes_lop3_peak", "tdes_device_geometry")
+           "tdes_count_mismatch", "tdes_lop3_peak", "tdes_device_geometry", "tdes_paper_ecb")
 
 
 def _check(rc: int, what: str):
@@ -226,6 +227,27 @@ def device_geometry() -> tuple[int, int]:
     a, b = ctypes.c_int(), ctypes.c_int()
     _check(_lib.tdes_device_geometry(ctypes.byref(a), ctypes.byref(b)), "tdes_device_geometry")
     return a.value, b.value
+
+
+class PaperBaseline:
+    """The paper's own kernel design on this GPU (include/tdes_paper.h; comparison only).
+
+    Key-generation kernel (3 CTAs x 56 threads) + three launches of a
+    64-thread-CTA-per-block, char-per-bit crypt kernel (§IV).
+    """
+
+    def __init__(self, k1, k2, k3, device=None):
+        dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        keys = _key_bytes(k1) + _key_bytes(k2) + _key_bytes(k3)
+        self.keys = torch.tensor(list(keys), dtype=torch.uint8, device=dev)
+        self.workspace = torch.empty(3 * 16 * 48, dtype=torch.uint8, device=dev)
+
+    def run(self, x: torch.Tensor, decrypt=False, out=None, stream=None):
+        out = _prep(x, out)
+        _check(_lib.tdes_paper_ecb(self.keys.data_ptr(), x.data_ptr(), out.data_ptr(), x.numel() // 8,
+                                   int(bool(decrypt)), self.workspace.data_ptr(), self.workspace.numel(),
+                                   _stream_handle(stream)), "tdes_paper_ecb")
+        return out
 
 
 # ------------------------------------------------------ bench helpers -----

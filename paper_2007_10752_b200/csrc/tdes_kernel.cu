@@ -35,14 +35,54 @@ constexpr int kTileBlocks = 32 * kBlocksPerThread;  // per warp: 1024 blocks = 8
 
 thread_local int g_last_cuda_error = 0;
 
+// mulhi.s32(0x7FFFFFFF, s) = (s - 1) / 2 for s = +-1 (tdes_gen::kxor).  Passed
+// as a kernel argument so it lives in a register instead of being folded into
+// an immediate (which would force s out of the uniform datapath).
+constexpr uint32_t kMulhiC = 0x7FFFFFFFu;
+
 // Launch-parameter key material, consumption order (round, E-bit):
-//   k = all-ones / all-zeros lane mask of the subkey bit, s = k | 1 (+1 or -1),
-// so that the key XOR runs as one IMAD x * s + k (tdes_gen::kxor).
+// s = k | 1 (+1 or -1) where k is the subkey bit's all-ones / all-zeros lane
+// mask; the key XOR is rebuilt from s on the FMA pipe (tdes_gen::kxor).
 template <int NROUNDS>
 struct RoundMasks {
   uint32_t s[NROUNDS][48];
-  uint32_t k[NROUNDS][48];
+  uint32_t k[NROUNDS][48];  // read only by the MULHI = false key XOR
 };
+
+// Key-XOR form per variant (tdes_gen::kxor): measured on B200, the loaded-k
+// form is 9% faster for 3DES; for single DES ptxas emits 32-bit per-thread
+// loads for k that saturate the ADU pipe, and rebuilding k from s is 1.9x faster.
+template <int NSTAGES>
+constexpr bool kUseMulhi = NSTAGES == 1;
+
+// x >> s as the high word of x * 2^(32-s): IMAD.HI on the FMA pipe instead of
+// SHF on the integer ALU pipe (the kernel's bound).  Left shifts already
+// compile to IMAD.SHL.
+#ifndef TDES_SHR_FMA
+#define TDES_SHR_FMA 1
+#endif
+template <int S>
+__device__ __forceinline__ uint32_t shr_fma(uint32_t x) {
+#if TDES_SHR_FMA
+  uint32_t d;
+  asm("mul.hi.u32 %0, %1, %2;" : "=r"(d) : "r"(x), "n"(1u << (32 - S)));
+  return d;
+#else
+  return x >> S;
+#endif
+}
+
+// One bit-level transpose stage: swap bit S of the row and column index.
+template <int S>
+__device__ __forceinline__ void bitstage(uint32_t (&a)[32], uint32_t m) {
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    if (k & S) continue;
+    const uint32_t lo = a[k], hi = a[k + S];
+    a[k] = tdes_gen::lop3<0xCA>(m, lo, hi << S);            // m ? lo : (hi << S)
+    a[k + S] = tdes_gen::lop3<0xCA>(m, shr_fma<S>(lo), hi);  // m ? (lo >> S) : hi
+  }
+}
 
 // In-register 32x32 bit-matrix transpose: a[i] bit j <-> a[j] bit i.
 // Stage s swaps bit s of the row and column index; s = 16 and 8 are whole
@@ -61,24 +101,17 @@ __device__ __forceinline__ void transpose32(uint32_t (&a)[32]) {
     a[k] = __byte_perm(lo, hi, 0x6240);
     a[k + 8] = __byte_perm(lo, hi, 0x7351);
   }
-#pragma unroll
-  for (int s = 4; s >= 1; s >>= 1) {
-    const uint32_t m = s == 4 ? 0x0F0F0F0Fu : s == 2 ? 0x33333333u : 0x55555555u;
-#pragma unroll
-    for (int k = 0; k < 32; ++k) {
-      if (k & s) continue;
-      const uint32_t lo = a[k], hi = a[k + s];
-      a[k] = tdes_gen::lop3<0xCA>(m, lo, hi << s);        // m ? lo : (hi << s)
-      a[k + s] = tdes_gen::lop3<0xCA>(m, lo >> s, hi);    // m ? (lo >> s) : hi
-    }
-  }
+  bitstage<4>(a, 0x0F0F0F0Fu);
+  bitstage<2>(a, 0x33333333u);
+  bitstage<1>(a, 0x55555555u);
 }
 
 // One warp tile: 32 lanes x 32 blocks = 1024 consecutive blocks from `base`.
 // VEC4: in/out 16-byte aligned -> 128-bit accesses (2 blocks per access).
 template <int NSTAGES, bool VEC4>
 __device__ __forceinline__ void crypt_tile(const uint2* in, uint2* out, size_t base, size_t nblocks,
-                                           unsigned lane, const RoundMasks<16 * NSTAGES>& mk) {
+                                           unsigned lane, const RoundMasks<16 * NSTAGES>& mk,
+                                           uint32_t c) {
   const bool full = base + kTileBlocks <= nblocks;
   uint32_t X[32], Y[32];
   // ---- S1: load.  Plane bit i <-> the i-th block this lane loads. ----
@@ -130,8 +163,8 @@ __device__ __forceinline__ void crypt_tile(const uint2* in, uint2* out, size_t b
 #pragma unroll 1
   for (int r = 0; r < 16 * NSTAGES; r += 2) {
     if (NSTAGES == 3 && (r == 16 || r == 32)) tdes_gen::swap_halves(P);
-    tdes_gen::round_A(P, mk.s[r], mk.k[r]);
-    tdes_gen::round_B(P, mk.s[r + 1], mk.k[r + 1]);
+    tdes_gen::round_A<kUseMulhi<NSTAGES>>(P, mk.s[r], mk.k[r], c);
+    tdes_gen::round_B<kUseMulhi<NSTAGES>>(P, mk.s[r + 1], mk.k[r + 1], c);
   }
   uint32_t Q[64];
   tdes_gen::output_planes(P, Q);
@@ -173,7 +206,7 @@ __device__ __forceinline__ void crypt_tile(const uint2* in, uint2* out, size_t b
 template <int NSTAGES, bool VEC4>
 __global__ void __launch_bounds__(kThreads, kMinCtasPerSm)
 tdes_ecb_kernel(const uint2* in, uint2* out, size_t nblocks,
-                const __grid_constant__ RoundMasks<16 * NSTAGES> mk) {
+                const __grid_constant__ RoundMasks<16 * NSTAGES> mk, uint32_t c) {
   __shared__ unsigned int next_tile;
   const unsigned lane = threadIdx.x & 31u;
   const size_t ntiles = (nblocks + kTileBlocks - 1) / kTileBlocks;
@@ -186,7 +219,7 @@ tdes_ecb_kernel(const uint2* in, uint2* out, size_t nblocks,
     if (lane == 0) t = atomicAdd(&next_tile, 1u);
     const size_t tile = lo + __shfl_sync(0xffffffffu, t, 0);
     if (tile >= hi) break;
-    crypt_tile<NSTAGES, VEC4>(in, out, tile * kTileBlocks, nblocks, lane, mk);
+    crypt_tile<NSTAGES, VEC4>(in, out, tile * kTileBlocks, nblocks, lane, mk, c);
   }
 }
 
@@ -242,9 +275,8 @@ int launch(const uint32_t (*masks)[48], const void* in, void* out, size_t nblock
   RoundMasks<16 * NSTAGES> mk;
   for (int r = 0; r < 16 * NSTAGES; ++r)
     for (int b = 0; b < 48; ++b) {
-      const uint32_t m = masks[r][b] ? 0xFFFFFFFFu : 0u;
-      mk.k[r][b] = m;
-      mk.s[r][b] = m | 1u;
+      mk.s[r][b] = masks[r][b] ? 0xFFFFFFFFu : 1u;  // s = k | 1
+      mk.k[r][b] = masks[r][b] ? 0xFFFFFFFFu : 0u;
     }
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -259,9 +291,9 @@ int launch(const uint32_t (*masks)[48], const void* in, void* out, size_t nblock
   const uint2* pin = static_cast<const uint2*>(in);
   uint2* pout = static_cast<uint2*>(out);
   if (vec4)
-    tdes_ecb_kernel<NSTAGES, true><<<grid, kThreads, 0, stream>>>(pin, pout, nblocks, mk);
+    tdes_ecb_kernel<NSTAGES, true><<<grid, kThreads, 0, stream>>>(pin, pout, nblocks, mk, kMulhiC);
   else
-    tdes_ecb_kernel<NSTAGES, false><<<grid, kThreads, 0, stream>>>(pin, pout, nblocks, mk);
+    tdes_ecb_kernel<NSTAGES, false><<<grid, kThreads, 0, stream>>>(pin, pout, nblocks, mk, kMulhiC);
   e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e);
   return TDES_OK;

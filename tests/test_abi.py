@@ -22,7 +22,7 @@ def tdes():
 
 def declared_functions():
     names = set()
-    for h in ("tdes.h", "tdes_bench.h"):
+    for h in ("tdes.h", "tdes_bench.h", "tdes_paper.h"):
         txt = open(os.path.join(ROOT, "include", h)).read()
         txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
         for m in re.finditer(r"^\s*(?:const\s+)?[A-Za-z_][A-Za-z_0-9]*\s*\*?\s*([a-z_0-9]+)\s*\(", txt, re.M):

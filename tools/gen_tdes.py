@@ -224,11 +224,14 @@ def emit_round(half):
     for i, m in enumerate(P_SRC):
         pinv[m] = i
     lines = [f"// One Feistel round updating half {half}: {half} ^= P(S(E(other) ^ K)).",
-             "// Key XOR on the FMA pipe: with k in {0, ~0} and s = k | 1, x ^ k == x * s + k.",
+             "// Key XOR on the FMA pipe (kxor): S = the round's 48 s = k | 1 values, K = the",
+             "// masks k (read only when MULHI = false), c = 0x7FFFFFFF.",
+             "template <bool MULHI>",
              f"__device__ __forceinline__ void round_{half}(uint32_t (&P)[64], const uint32_t* __restrict__ S,",
-             "                                        const uint32_t* __restrict__ K) {"]
+             "                                        const uint32_t* __restrict__ K, uint32_t c) {"]
     for g in range(8):
-        xs = [f"kxor(P[{src[T.E[6 * g + i] - 1]}], S[{6 * g + i}], K[{6 * g + i}])" for i in range(6)]
+        xs = [f"kxor<MULHI>(P[{src[T.E[6 * g + i] - 1]}], S[{6 * g + i}], MULHI ? 0u : K[{6 * g + i}], c)"
+              for i in range(6)]
         lines.append("  { uint32_t o0, o1, o2, o3;")
         lines.append(f"    sbox{g + 1}({', '.join(xs)}, o0, o1, o2, o3);")
         for o in range(4):
@@ -256,11 +259,22 @@ def emit_header(circs):
 
         f"constexpr int kSboxLop3[8] = {{{', '.join(str(len(c['gates'])) for c in circs)}}};",
         "",
-        "// x ^ k for a lane mask k in {0, 0xFFFFFFFF}, given s = k | 1 (= +1 or -1):",
-        "// x * s + k is x (k = 0) or -x - 1 = ~x (k = ~0).  One IMAD on the FMA pipe,",
-        "// leaving the integer ALU pipe (the kernel's bound) to the S-box LOP3s.",
-        "__device__ __forceinline__ uint32_t kxor(uint32_t x, uint32_t s, uint32_t k) {",
-        "  uint32_t d;",
+        "// x ^ k for a lane mask k in {0, 0xFFFFFFFF}, on the FMA pipe (the integer ALU",
+        "// pipe, the kernel's bound, stays with the S-box LOP3s).  With s = k | 1 (+1/-1):",
+        "//   x ^ k = x * s + k             (x for k = 0, -x - 1 = ~x for k = ~0)",
+        "// MULHI = true: k is rebuilt from s as mulhi.s32(c = 0x7FFFFFFF, s), so only s is",
+        "//   loaded (uniform LDCU); two IMADs per key bit.",
+        "// MULHI = false: k is loaded too (ptxas uses per-thread LDC.64); one IMAD.",
+        "// Which is faster depends on ptxas's code for the variant (measured: false for",
+        "// 3DES, true for single DES, where the loads were 32-bit and saturated the ADU).",
+        "template <bool MULHI>",
+        "__device__ __forceinline__ uint32_t kxor(uint32_t x, uint32_t s, uint32_t kmem, uint32_t c) {",
+        "  uint32_t k, d;",
+        "  if (MULHI) {",
+        "    asm(\"mul.hi.s32 %0, %1, %2;\" : \"=r\"(k) : \"r\"(c), \"r\"(s));",
+        "  } else {",
+        "    k = kmem;",
+        "  }",
         "  asm(\"mad.lo.u32 %0, %1, %2, %3;\" : \"=r\"(d) : \"r\"(x), \"r\"(s), \"r\"(k));",
         "  return d;",
         "}",
@@ -314,6 +328,22 @@ def emit_host_tables():
     ])
 
 
+def emit_paper_tables():
+    """Device tables for the paper-faithful comparison kernel (csrc/tdes_paper_kernel.cu)."""
+    T.check()
+
+    def arr(name, vals):
+        return f"__device__ const uint8_t {name}[{len(vals)}] = {{{', '.join(map(str, vals))}}};"
+    sbox = [v for box in T.SBOX for row in box for v in row]
+    return "\n".join([
+        "// GENERATED by tools/gen_tdes.py from tools/des_tables.py -- do not edit.",
+        "// Appendix A tables (PAPER.md:208-353), 1-based, for the read-only path (P:128).",
+        "#pragma once",
+        arr("d_pc1", T.PC1), arr("d_pc2", T.PC2), arr("d_ip", T.IP), arr("d_e", T.E),
+        arr("d_sbox", sbox), arr("d_p", T.P), arr("d_fp", T.FP), "",
+    ])
+
+
 def manifest(circs):
     return {
         "sbox_lop3": [len(c["gates"]) for c in circs],
@@ -336,6 +366,7 @@ def main(argv=None):
     files = {
         "tdes_gen.cuh": emit_header(circs),
         "tdes_host_tables.h": emit_host_tables(),
+        "tdes_paper_tables.cuh": emit_paper_tables(),
         "manifest.json": json.dumps(manifest(circs), indent=1) + "\n",
     }
     for name, text in files.items():

@@ -46,6 +46,14 @@ def main():
         ms = time_it(lambda: tdes.ecb_encrypt(x, s, out=y))
         print(f"3DES enc 2^{e} blocks: {ms:.3f} ms  {n * 8 / ms / 1e6:.1f} GB/s  {n / ms / 1e6:.3f} Gblk/s")
         del x, y
+    base = tdes.PaperBaseline(*synthetic.KEYS_3KEY)
+    for e in (17, 20, 23):
+        n = 1 << e
+        x = torch.empty(8 * n, dtype=torch.uint8, device="cuda")
+        tdes.fill_splitmix64(x)
+        y = torch.empty_like(x)
+        ms = time_it(lambda: base.run(x, out=y), reps=5)
+        print(f"paper-design kernel 2^{e} blocks: {ms:.3f} ms  {n * 8 / ms / 1e6:.2f} GB/s")
     ds = tdes.des_key_schedule(synthetic.KEYS_1KEY[0])
     n = 1 << 27
     x = torch.empty(8 * n, dtype=torch.uint8, device="cuda")
