@@ -77,9 +77,18 @@ def emulate(man, circs, blocks_u8, masks):
             for lut, a, b, c in circs[g]["gates"]:
                 sig.append(lut_np(lut, sig[a], sig[b], sig[c]))
             neg = circs[g].get("neg") or [0, 0, 0, 0]
+            fuse = circs[g].get("fuse") or [None] * 4
             for o in range(4):
-                v = sig[circs[g]["outputs"][o]]
-                upd[dst[pinv[4 * g + o]]] = ~v if neg[o] else v
+                if fuse[o] is not None:
+                    fu, fv, h = fuse[o]
+                    v = np.zeros_like(sig[fu])
+                    for q in range(4):
+                        if (h >> q) & 1:
+                            v |= (sig[fu] if q & 2 else ~sig[fu]) & (sig[fv] if q & 1 else ~sig[fv])
+                else:
+                    v = sig[circs[g]["outputs"][o]]
+                    v = ~v if neg[o] else v
+                upd[dst[pinv[4 * g + o]]] = v
         for d, v in upd.items():
             P[d] = P[d] ^ v
     Q = [P[man["out_src"][k]] for k in range(64)]

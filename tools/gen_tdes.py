@@ -77,7 +77,31 @@ def eval_circuit(circ, inputs=None, full=FULL):
     for lut, a, b, c in circ["gates"]:
         sig.append(lut_eval(lut, sig[a], sig[b], sig[c], full))
     neg = circ.get("neg") or [0, 0, 0, 0]
-    return [sig[s] ^ (full if n else 0) for s, n in zip(circ["outputs"], neg)]
+    fuse = circ.get("fuse") or [None] * 4
+    out = []
+    for s, n, f in zip(circ["outputs"], neg, fuse):
+        if f is not None:   # 2-input output h(u, v), h index = (u << 1) | v
+            u, v, h = f
+            out.append(fused_eval(h, sig[u], sig[v], full))
+        else:
+            out.append(sig[s] ^ (full if n else 0))
+    return out
+
+
+def fused_eval(h: int, u: int, v: int, full: int = FULL) -> int:
+    """h(u, v) bitwise for a 4-bit table h indexed by (u << 1) | v."""
+    r = 0
+    for q in range(4):
+        if (h >> q) & 1:
+            r |= (u if q & 2 else ~u) & (v if q & 1 else ~v)
+    return r & full
+
+
+def circuit_cost(circ) -> int:
+    """ALU LOP3s per S-box per round: the gates plus one LOP3 per output into its
+    destination plane (a plain XOR/XNOR, or a fused LOP3(P, u, v) when the output
+    is a 2-input function h(u, v) of two signals -- then that join needs no gate)."""
+    return len(circ["gates"]) + 4
 
 
 def verify_circuit(g: int, circ) -> bool:
@@ -85,6 +109,12 @@ def verify_circuit(g: int, circ) -> bool:
         return False
     for k, (lut, a, b, c) in enumerate(circ["gates"]):
         if not (0 <= lut <= 255 and max(a, b, c) < 6 + k and min(a, b, c) >= 0):
+            return False
+    n = 6 + len(circ["gates"])
+    for s, f in zip(circ["outputs"], circ.get("fuse") or [None] * 4):
+        if f is None and not 0 <= s < n:
+            return False
+        if f is not None and not (0 <= f[0] < n and 0 <= f[1] < n and 0 <= f[2] < 16):
             return False
     return eval_circuit(circ) == [sbox_tt(g, o) for o in range(4)]
 
@@ -132,11 +162,12 @@ def load_searched():
         for item in data.get("circuits", []):
             g = item["sbox"]
             circ = {"gates": item["gates"], "outputs": item["outputs"],
-                    "neg": item.get("neg", [0, 0, 0, 0]), "source": os.path.basename(path)}
+                    "neg": item.get("neg", [0, 0, 0, 0]), "fuse": item.get("fuse") or [None] * 4,
+                    "source": os.path.basename(path)}
             if not verify_circuit(g, circ):
                 print(f"warning: {path} S{g + 1} circuit fails verification; ignored", file=sys.stderr)
                 continue
-            if g not in best or len(circ["gates"]) < len(best[g]["gates"]):
+            if g not in best or circuit_cost(circ) < circuit_cost(best[g]):
                 best[g] = circ
     return best
 
@@ -148,7 +179,7 @@ def choose_circuits(muxtree_only=False):
         m = muxtree_circuit(g)
         assert verify_circuit(g, m)
         c = searched.get(g)
-        out.append(c if c is not None and len(c["gates"]) < len(m["gates"]) else m)
+        out.append(c if c is not None and circuit_cost(c) < circuit_cost(m) else m)
     return out
 
 
@@ -199,11 +230,20 @@ def round_schedule():
 # ------------------------------------------------------------------ emitter --
 
 
+def fused_lut(h: int) -> int:
+    """LOP3 table of d ^ h(u, v) over inputs (a = d, b = u, c = v)."""
+    return sum(1 << k for k in range(8) if ((k >> 2) & 1) ^ ((h >> (k & 3)) & 1))
+
+
 def emit_sbox(g, circ):
-    lines = [f"// S{g + 1}: {len(circ['gates'])} lop3 ({circ['source']})",
+    fuse = circ.get("fuse") or [None] * 4
+    nf = sum(1 for f in fuse if f is not None)
+    lines = [f"// S{g + 1}: {len(circ['gates'])} lop3 + 4 Feistel XOR ({nf} of them fused with the output's"
+             f" final 2-input join) = {circuit_cost(circ)} ALU ops ({circ['source']})",
+             "// Inputs x0..x5 = S-box bits b1..b6; each output is XORed into its destination plane.",
              f"__device__ __forceinline__ void sbox{g + 1}(uint32_t x0, uint32_t x1, uint32_t x2, "
              "uint32_t x3, uint32_t x4, uint32_t x5,",
-             "    uint32_t& o0, uint32_t& o1, uint32_t& o2, uint32_t& o3) {"]
+             "    uint32_t& d0, uint32_t& d1, uint32_t& d2, uint32_t& d3) {"]
 
     def name(s):
         return f"x{s}" if s < 6 else f"t{s - 6}"
@@ -211,8 +251,13 @@ def emit_sbox(g, circ):
         lines.append(f"  const uint32_t t{k} = lop3<0x{lut:02x}>({name(a)}, {name(b)}, {name(c)});")
     neg = circ.get("neg") or [0, 0, 0, 0]
     for o, s in enumerate(circ["outputs"]):
-        # a complemented output costs nothing: the Feistel XOR becomes an XNOR (one LOP3)
-        lines.append(f"  o{o} = {'~' if neg[o] else ''}{name(s)};")
+        f = fuse[o]
+        if f is not None:
+            lines.append(f"  d{o} = lop3<0x{fused_lut(f[2]):02x}>(d{o}, {name(f[0])}, {name(f[1])});"
+                         f"  // d ^= h(u, v), h = 0x{f[2]:x}")
+        else:
+            # a complemented output costs nothing: the XOR becomes an XNOR (one LOP3)
+            lines.append(f"  d{o} ^= {'~' if neg[o] else ''}{name(s)};")
     lines.append("}")
     return "\n".join(lines)
 
@@ -232,11 +277,9 @@ def emit_round(half):
     for g in range(8):
         xs = [f"kxor<MULHI>(P[{src[T.E[6 * g + i] - 1]}], S[{6 * g + i}], MULHI ? 0u : K[{6 * g + i}], c)"
               for i in range(6)]
-        lines.append("  { uint32_t o0, o1, o2, o3;")
-        lines.append(f"    sbox{g + 1}({', '.join(xs)}, o0, o1, o2, o3);")
-        for o in range(4):
-            lines.append(f"    P[{dst[pinv[4 * g + o]]}] ^= o{o};")
-        lines.append("  }")
+        ds = [f"P[{dst[pinv[4 * g + o]]}]" for o in range(4)]
+        lines.append(f"  sbox{g + 1}({', '.join(xs)},")
+        lines.append(f"        {', '.join(ds)});")
     lines.append("}")
     return "\n".join(lines)
 
@@ -256,6 +299,8 @@ def emit_header(circs):
         "namespace tdes_gen {",
         "",
         f"constexpr int kSboxLop3Total = {total};",
+        "// ALU ops per round for the S-boxes including the Feistel XORs (fused or not)",
+        f"constexpr int kRoundAluOps = {sum(circuit_cost(c) for c in circs)};",
 
         f"constexpr int kSboxLop3[8] = {{{', '.join(str(len(c['gates'])) for c in circs)}}};",
         "",
@@ -349,8 +394,10 @@ def manifest(circs):
         "sbox_lop3": [len(c["gates"]) for c in circs],
         "sbox_lop3_total": sum(len(c["gates"]) for c in circs),
         "sources": [c["source"] for c in circs],
+        "round_alu_ops": sum(circuit_cost(c) for c in circs),
         "circuits": [{"sbox": g, "gates": c["gates"], "outputs": c["outputs"],
-                      "neg": c.get("neg") or [0, 0, 0, 0]} for g, c in enumerate(circs)],
+                      "neg": c.get("neg") or [0, 0, 0, 0], "fuse": c.get("fuse") or [None] * 4}
+                     for g, c in enumerate(circs)],
         "a_idx": A_IDX, "b_idx": B_IDX, "p_src": P_SRC, "out_src": OUT_SRC,
         "round_schedule": round_schedule(),
     }
@@ -376,7 +423,9 @@ def main(argv=None):
             with open(path, "w") as f:
                 f.write(text)
     print("S-box LOP3 per box:", [len(c["gates"]) for c in circs],
-          "total", sum(len(c["gates"]) for c in circs))
+          "total", sum(len(c["gates"]) for c in circs),
+          "| round ALU ops incl. Feistel XOR:", [circuit_cost(c) for c in circs],
+          "total", sum(circuit_cost(c) for c in circs))
 
 
 if __name__ == "__main__":

@@ -38,7 +38,7 @@ def load():
 def save(best):
     os.makedirs(os.path.dirname(OUT), exist_ok=True)
     data = {"generator": "tools/sbox_search/sbox_search.c (Kwan-style LUT3 decomposition search)",
-            "total": sum(len(best[g]["gates"]) for g in sorted(best)),
+            "total_cost": sum(gen_tdes.circuit_cost(best[g]) for g in sorted(best)),
             "circuits": [best[g] for g in sorted(best)]}
     with open(OUT, "w") as f:
         json.dump(data, f, indent=1)
@@ -64,17 +64,20 @@ def main():
             print(f"S{g + 1}: no circuit")
             continue
         circ = {"sbox": g, "gates": d["gates"], "outputs": d["outputs"], "neg": d["neg"],
-                "source": "lut3_search"}
+                "fuse": d.get("fuse") or [None] * 4, "source": "lut3_search"}
         ok = gen_tdes.verify_circuit(g, circ)
         old = best.get(g)
-        n = len(d["gates"])
-        msg = f"S{g + 1}: {n} gates ({time.time() - t0:.1f}s) verified={ok} prev={len(old['gates']) if old else None}"
-        if ok and (old is None or n < len(old["gates"])):
+        n = gen_tdes.circuit_cost(circ)
+        prev = gen_tdes.circuit_cost(old) if old else None
+        msg = (f"S{g + 1}: cost {n} ({len(d['gates'])} gates, {sum(f is not None for f in circ['fuse'])} fused)"
+               f" ({time.time() - t0:.1f}s) verified={ok} prev={prev}")
+        if ok and (old is None or n < prev):
             best[g] = circ
             save(best)
             msg += " NEW BEST"
         print(msg, flush=True)
-    print("total", sum(len(best[g]["gates"]) for g in best), [len(best[g]["gates"]) for g in sorted(best)])
+    print("total cost", sum(gen_tdes.circuit_cost(best[g]) for g in best),
+          [gen_tdes.circuit_cost(best[g]) for g in sorted(best)])
 
 
 if __name__ == "__main__":

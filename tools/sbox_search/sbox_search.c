@@ -25,7 +25,9 @@
  * value, truth-table bit v has x_i = bit (5-i) of v); signal 6+k is gate k.
  *
  * Usage: sbox_search <trials> <seed> <levels> <t0> <t1> <t2> <t3>
- *        levels = full_levels + 10 * all_forms (all_forms: try AND/OR join forms too)
+ *        levels = full_levels + 10 * all_forms + 100 * fuse
+ *        (all_forms: try AND/OR join forms too; fuse: fold the Feistel XOR into
+ *        2-input output joins, minimizing gates + unfused outputs)
  *        (t_o = 64-bit truth table of output bit o, hex)
  * The result is verified exhaustively by the caller (tools/run_sbox_search.py)
  * and again by tools/gen_tdes.py before any code is emitted.
@@ -122,6 +124,7 @@ static int find_single(St *s, tt_t T, tt_t M, uint64_t *rng) {
 typedef struct {
   int full_levels;
   int all_forms;
+  int fuse;
 } Cfg;
 
 static int create(St *s, tt_t T, tt_t M, int selused, int level, const Cfg *cfg, uint64_t *rng,
@@ -228,10 +231,117 @@ static int create(St *s, tt_t T, tt_t M, int selused, int level, const Cfg *cfg,
   return bestg;
 }
 
+/* Per output: either a plain signal (out, neg; the kernel XORs it into the
+ * other half with one LOP3), or -- fused mode -- a 2-input function fh(fu, fv)
+ * (4-bit table, index (u<<1)|v) folded into that same LOP3: P ^= fh(u, v) is
+ * LOP3(P, u, v).  Either way each output costs exactly one LOP3 into P, so the
+ * cost of a circuit is its gate count (ALU ops per S-box per round = gates + 4);
+ * fusion pays off when an output's final join is 2-input and needs no gate. */
 typedef struct {
   St s;
   int out[4], neg[4];
+  int fu[4], fv[4], fh[4];
+  int cost;
 } Result;
+
+/* 2-input table h with h(U, V) = T on M, or -1 */
+static inline int fit2(tt_t U, tt_t V, tt_t T, tt_t M) {
+  int h = 0;
+  const tt_t r[4] = {M & ~U & ~V, M & ~U & V, M & U & ~V, M & U & V};
+  for (int q = 0; q < 4; q++) {
+    const tt_t t = T & r[q];
+    if (t && t != r[q]) return -1;
+    if (t) h |= 1 << q;
+  }
+  return h;
+}
+
+typedef struct {
+  int plain, g, neg, u, v, h, cost;
+} OutChoice;
+
+/* Try to realize T on the full space as a fused 2-input join h(f0, f1):
+ * f0 = T on the x_i = first half, then f1 from the form:
+ *   0 XOR  f1 = T ^ f0 everywhere
+ *   1 OR   f1 = T where f0 = 0 (needs f0 => T); free where f0 = 1 (or T = 1 on the first half)
+ *   2 AND  f1 = T where f0 = 1 (needs T => f0); free where f0 = 0 */
+static int try_fused(St *s, tt_t T, int i, int first, int form, const Cfg *cfg, uint64_t *rng,
+                     OutChoice *oc) {
+  const tt_t X = first ? VARS[i] : ~VARS[i];
+  const int n_before = s->n;
+  int n0, n1;
+  const int f0 = create(s, T, X, 1 << i, 1, cfg, rng, &n0);
+  if (f0 < 0) return -1;
+  const tt_t F = s->tt[f0] ^ (n0 ? ~0ull : 0ull); /* == T on X */
+  tt_t T1 = T, K1 = ~0ull;
+  switch (form) {
+    case 0: T1 = T ^ F; break;
+    case 1: if (F & ~T & ~X) return -1; K1 = (X & ~T) | (~X & ~F); break;
+    case 2: if (T & ~F & ~X) return -1; K1 = (X & T) | (~X & F); break;
+  }
+  int f1;
+  if (!K1) f1 = f0, n1 = 0;
+  else f1 = create(s, T1, K1, 0, 1, cfg, rng, &n1);
+  if (f1 < 0) return -1;
+  const int h = fit2(s->tt[f0], s->tt[f1], T, ~0ull);
+  if (h < 0) return -1;
+  oc->plain = 0;
+  oc->u = f0;
+  oc->v = f1;
+  oc->h = h;
+  oc->cost = s->n - n_before;
+  return 0;
+}
+
+/* Build output target T choosing the cheapest of: an existing signal (+1 XOR),
+ * a 2-input function of two existing signals (fused, +0), fused Shannon joins,
+ * or a plain build (+1 XOR).  Leaves the chosen construction in *s. */
+static int create_output(St *s, tt_t T, const Cfg *cfg, uint64_t *rng, OutChoice *best) {
+  int neg;
+  best->cost = 1 << 20;
+  /* existing pair -> fused, free */
+  const int n = s->n;
+  for (int u = 0; u < n; u++)
+    for (int v = u + 1; v < n; v++) {
+      const int h = fit2(s->tt[u], s->tt[v], T, ~0ull);
+      if (h >= 0) {
+        best->plain = 0, best->u = u, best->v = v, best->h = h, best->cost = 0;
+        return 0;
+      }
+    }
+  int g = find_existing(s, T, ~0ull, &neg);
+  if (g >= 0) {
+    best->plain = 1, best->g = g, best->neg = neg, best->cost = 1;
+    return 0;
+  }
+  St *bestst = (St *)malloc(sizeof(St)), *tmp = (St *)malloc(sizeof(St));
+  int have = 0;
+  /* plain build */
+  memcpy(tmp, s, sizeof(St));
+  g = create(tmp, T, ~0ull, 0, 0, cfg, rng, &neg);
+  if (g >= 0) {
+    best->plain = 1, best->g = g, best->neg = neg, best->cost = tmp->n - s->n;
+    memcpy(bestst, tmp, sizeof(St));
+    have = 1;
+  }
+  /* fused Shannon joins */
+  for (int i = 0; i < 6; i++)
+    for (int first = 0; first < 2; first++)
+      for (int form = 0; form < 3; form++) {
+        OutChoice oc;
+        memcpy(tmp, s, sizeof(St));
+        if (try_fused(tmp, T, i, first, form, cfg, rng, &oc) < 0) continue;
+        if (oc.cost < best->cost || (oc.cost == best->cost && (rnd(rng) & 1))) {
+          *best = oc;
+          memcpy(bestst, tmp, sizeof(St));
+          have = 1;
+        }
+      }
+  if (have) memcpy(s, bestst, sizeof(St));
+  free(bestst);
+  free(tmp);
+  return have ? 0 : -1;
+}
 
 static void run_trial(const tt_t targets[4], const Cfg *cfg, uint64_t seed, Result *res) {
   uint64_t rng = seed;
@@ -246,8 +356,24 @@ static void run_trial(const tt_t targets[4], const Cfg *cfg, uint64_t seed, Resu
     order[k] = order[j];
     order[j] = t;
   }
+  int unfused = 0;
   for (int q = 0; q < 4; q++) {
     const int o = order[q];
+    res->fh[o] = -1;
+    if (cfg->fuse) {
+      OutChoice oc;
+      if (create_output(s, targets[o], cfg, &rng, &oc) < 0) {
+        s->n = MAXG + 1;
+        return;
+      }
+      if (oc.plain) {
+        res->out[o] = oc.g, res->neg[o] = oc.neg, unfused++;
+      } else {
+        res->out[o] = -1, res->neg[o] = 0;
+        res->fu[o] = oc.u, res->fv[o] = oc.v, res->fh[o] = oc.h;
+      }
+      continue;
+    }
     int ng = 0;
     const int g = create(s, targets[o], ~0ull, 0, 0, cfg, &rng, &ng);
     if (g < 0) {
@@ -256,14 +382,20 @@ static void run_trial(const tt_t targets[4], const Cfg *cfg, uint64_t seed, Resu
     }
     res->out[o] = g;
     res->neg[o] = ng;
+    unfused++;
   }
+  (void)unfused;
+  res->cost = s->n - 6;
 }
 
 /* remove gates not reachable from the outputs, renumber */
 static void prune(Result *r) {
   St *s = &r->s;
   int live[MAXG] = {0};
-  for (int o = 0; o < 4; o++) live[r->out[o]] = 1;
+  for (int o = 0; o < 4; o++) {
+    if (r->fh[o] >= 0) live[r->fu[o]] = live[r->fv[o]] = 1;
+    else live[r->out[o]] = 1;
+  }
   for (int g = s->n - 1; g >= 6; g--)
     if (live[g])
       for (int j = 0; j < 3; j++) live[s->in[g][j]] = 1;
@@ -279,8 +411,18 @@ static void prune(Result *r) {
     if (!live[g]) continue;
     map[g] = add_gate(&t, s->lut[g], map[s->in[g][0]], map[s->in[g][1]], map[s->in[g][2]]);
   }
-  for (int o = 0; o < 4; o++) r->out[o] = map[r->out[o]];
+  int unfused = 0;
+  for (int o = 0; o < 4; o++) {
+    if (r->fh[o] >= 0) {
+      r->fu[o] = map[r->fu[o]], r->fv[o] = map[r->fv[o]];
+    } else {
+      r->out[o] = map[r->out[o]];
+      unfused++;
+    }
+  }
   memcpy(s, &t, sizeof t);
+  (void)unfused;
+  r->cost = s->n - 6;
 }
 
 int main(int argc, char **argv) {
@@ -290,7 +432,8 @@ int main(int argc, char **argv) {
   }
   const long trials = atol(argv[1]);
   const uint64_t seed = strtoull(argv[2], 0, 10);
-  Cfg cfg = {atoi(argv[3]) % 10, atoi(argv[3]) >= 10};
+  const int lv = atoi(argv[3]);
+  Cfg cfg = {lv % 10, (lv / 10) % 10 >= 1, lv >= 100};
   tt_t targets[4];
   for (int o = 0; o < 4; o++) targets[o] = strtoull(argv[4 + o], 0, 16);
   for (int i = 0; i < 6; i++) {
@@ -300,6 +443,7 @@ int main(int argc, char **argv) {
   }
   Result best;
   best.s.n = MAXG + 1;
+  best.cost = 1 << 20;
 #pragma omp parallel
   {
     Result *r = (Result *)malloc(sizeof(Result));
@@ -310,7 +454,7 @@ int main(int argc, char **argv) {
       prune(r);
 #pragma omp critical
       {
-        if (r->s.n < best.s.n) memcpy(&best, r, sizeof(Result));
+        if (r->cost < best.cost) memcpy(&best, r, sizeof(Result));
       }
     }
     free(r);
@@ -323,7 +467,12 @@ int main(int argc, char **argv) {
   for (int g = 6; g < best.s.n; g++)
     printf("%s[%d, %d, %d, %d]", g > 6 ? ", " : "", best.s.lut[g], best.s.in[g][0], best.s.in[g][1],
            best.s.in[g][2]);
-  printf("], \"outputs\": [%d, %d, %d, %d], \"neg\": [%d, %d, %d, %d]}\n", best.out[0], best.out[1],
-         best.out[2], best.out[3], best.neg[0], best.neg[1], best.neg[2], best.neg[3]);
+  printf("], \"outputs\": [%d, %d, %d, %d], \"neg\": [%d, %d, %d, %d], \"fuse\": [", best.out[0],
+         best.out[1], best.out[2], best.out[3], best.neg[0], best.neg[1], best.neg[2], best.neg[3]);
+  for (int o = 0; o < 4; o++) {
+    if (best.fh[o] >= 0) printf("%s[%d, %d, %d]", o ? ", " : "", best.fu[o], best.fv[o], best.fh[o]);
+    else printf("%snull", o ? ", " : "");
+  }
+  printf("], \"cost\": %d}\n", best.cost);
   return 0;
 }
