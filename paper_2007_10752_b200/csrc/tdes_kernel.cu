@@ -31,7 +31,11 @@ namespace {
 constexpr int kThreads = 512;        // 16 warps per CTA, one CTA per SM
 constexpr int kMinCtasPerSm = 1;     // => <= 128 registers per thread (64K-register file)
 constexpr int kBlocksPerThread = 32; // one bit-plane word
-constexpr int kTileBlocks = 32 * kBlocksPerThread;  // per warp: 1024 blocks = 8 KiB
+constexpr int kTileBlocks = 32 * kBlocksPerThread;
+#ifndef TDES_ROUND_UNROLL
+#define TDES_ROUND_UNROLL 1
+#endif
+constexpr int kRoundUnroll = TDES_ROUND_UNROLL;  // two-round loop bodies per iteration  // per warp: 1024 blocks = 8 KiB
 
 thread_local int g_last_cuda_error = 0;
 
@@ -160,7 +164,7 @@ __device__ __forceinline__ void crypt_tile(const uint2* in, uint2* out, size_t b
   // the instruction cache.  The middle stage starts on the half the first one
   // updated last, so at each stage boundary the halves swap
   // register roles and the same A-then-B body continues.
-#pragma unroll 1
+#pragma unroll kRoundUnroll
   for (int r = 0; r < 16 * NSTAGES; r += 2) {
     if (NSTAGES == 3 && (r == 16 || r == 32)) tdes_gen::swap_halves(P);
     tdes_gen::round_A<kUseMulhi<NSTAGES>>(P, mk.s[r], mk.k[r], c);
