@@ -45,6 +45,15 @@ int tdes_count_mismatch(const void *dev_a, const void *dev_b, size_t nblocks,
 int tdes_lop3_peak(uint32_t *dev_sink, int grid, int cta, int iters, uint64_t *ops_out,
                    tdes_stream_t stream);
 
+/* 3DES ECB with an explicit kernel choice (for measurement and tests):
+ *   mode 0  automatic (what tdes_ecb_encrypt/decrypt do: the S-box-split latency
+ *           kernel for small launches, the throughput kernel otherwise)
+ *   mode 1  throughput kernel (32 blocks per thread, one warp per 1024-block tile)
+ *   mode 2  S-box-split latency kernel (8 warps per tile, one S-box per warp)
+ * Same arguments and errors as tdes_ecb_encrypt; decrypt 0/1. */
+int tdes_ecb_crypt_mode(const tdes_schedule *s, int decrypt, const void *in, void *out,
+                        size_t nblocks, int mode, tdes_stream_t stream);
+
 /* Number of SMs of the current device and max resident CTAs/SM of the 3DES
  * kernel (its occupancy), for grid accounting. */
 int tdes_device_geometry(int *num_sms, int *ctas_per_sm);

@@ -77,6 +77,8 @@ def _load():
         "tdes_device_geometry": ([ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)],
                                  ctypes.c_int),
         "tdes_paper_ecb": ([vp, vp, vp, sz, ctypes.c_int, vp, sz, vp], ctypes.c_int),
+        "tdes_ecb_crypt_mode": ([ctypes.POINTER(TdesSchedule), ctypes.c_int, vp, vp, sz, ctypes.c_int, vp],
+                                ctypes.c_int),
     }
     for name, (argtypes, restype) in sig.items():
         fn = getattr(lib, name)
@@ -91,7 +93,10 @@ _lib = _load()
 EXPORTS = ("tdes_key_schedule", "tdes_ecb_encrypt", "tdes_ecb_decrypt", "des_key_schedule",
            "des_ecb_encrypt", "des_ecb_decrypt", "tdes_ecb_crypt_host", "tdes_get_kernel_info",
            "tdes_strerror", "tdes_last_cuda_error", "tdes_fill_splitmix64", "tdes_sum64",
-           "tdes_count_mismatch", "tdes_lop3_peak", "tdes_device_geometry", "tdes_paper_ecb")
+           "tdes_count_mismatch", "tdes_lop3_peak", "tdes_device_geometry", "tdes_paper_ecb",
+           "tdes_ecb_crypt_mode")
+
+MODE_AUTO, MODE_THROUGHPUT, MODE_SPLIT = 0, 1, 2
 
 
 def _check(rc: int, what: str):
@@ -176,6 +181,14 @@ def des_ecb_encrypt(x, sched: DesSchedule, out=None, stream=None):
 
 def des_ecb_decrypt(x, sched: DesSchedule, out=None, stream=None):
     return _crypt(_lib.des_ecb_decrypt, sched, x, out, stream, "des_ecb_decrypt")
+
+
+def ecb_crypt_mode(x: torch.Tensor, sched: TdesSchedule, mode: int, decrypt=False, out=None, stream=None):
+    """3DES ECB with an explicit kernel choice (MODE_AUTO / MODE_THROUGHPUT / MODE_SPLIT)."""
+    out = _prep(x, out)
+    _check(_lib.tdes_ecb_crypt_mode(ctypes.byref(sched), int(bool(decrypt)), x.data_ptr(), out.data_ptr(),
+                                    x.numel() // 8, mode, _stream_handle(stream)), "tdes_ecb_crypt_mode")
+    return out
 
 
 def ecb_encrypt_ptr(sched: TdesSchedule, in_ptr: int, out_ptr: int, nblocks: int, stream_handle: int = 0):

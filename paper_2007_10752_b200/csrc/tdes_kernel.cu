@@ -24,6 +24,7 @@
 #include <atomic>
 
 #include "../../include/tdes.h"
+#include "../../include/tdes_bench.h"
 #include "gen/tdes_gen.cuh"
 
 namespace {
@@ -31,11 +32,11 @@ namespace {
 constexpr int kThreads = 512;        // 16 warps per CTA, one CTA per SM
 constexpr int kMinCtasPerSm = 1;     // => <= 128 registers per thread (64K-register file)
 constexpr int kBlocksPerThread = 32; // one bit-plane word
-constexpr int kTileBlocks = 32 * kBlocksPerThread;
+constexpr int kTileBlocks = 32 * kBlocksPerThread;  // per warp: 1024 blocks = 8 KiB
 #ifndef TDES_ROUND_UNROLL
 #define TDES_ROUND_UNROLL 1
 #endif
-constexpr int kRoundUnroll = TDES_ROUND_UNROLL;  // two-round loop bodies per iteration  // per warp: 1024 blocks = 8 KiB
+constexpr int kRoundUnroll = TDES_ROUND_UNROLL;  // two-round bodies per loop iteration (2 measured 3% slower)
 
 thread_local int g_last_cuda_error = 0;
 
@@ -227,6 +228,108 @@ tdes_ecb_kernel(const uint2* in, uint2* out, size_t nblocks,
   }
 }
 
+// ------------------------------------------------ small-N latency mode -----
+// SURVEY NEXT-5.  With few tiles the main kernel runs each 1024-block tile on
+// one warp, so a launch lasts as long as one warp's 48 serial rounds.  Here a
+// team of 8 warps shares one tile: warp g evaluates S-box g (warp-uniform, no
+// divergence) for all 32 block-groups of the tile (lane l = group l), i.e. the
+// paper's idea of spreading one block's round over many threads,
+// applied at S-box granularity.  The 64 planes x 32 groups of state live in
+// shared memory (row stride 33 words: both the [group] and the [plane] access
+// patterns are bank-conflict free); every thread keeps the 4 planes of each
+// half that its S-box writes (P is a permutation, so these partition each
+// half) in registers and publishes them after each update; one barrier per
+// round.  Transposes are lane-parallel (5 shuffle butterfly stages).
+constexpr int kSplitThreads = 256;   // one team = 8 warps
+constexpr int kStride = 33;
+
+// 32x32 bit transpose across a warp: lane i holds row i on entry; on exit lane
+// j holds column j (bit i = entry lane i's bit j).  Stage s swaps bit s of the
+// lane index with bit s of the bit index.
+__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, unsigned lane) {
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) {
+    const uint32_t m0 = s == 16  ? 0x0000FFFFu
+                        : s == 8 ? 0x00FF00FFu
+                        : s == 4 ? 0x0F0F0F0Fu
+                        : s == 2 ? 0x33333333u
+                                 : 0x55555555u;  // bits whose index has bit s clear
+    const uint32_t y = __shfl_xor_sync(0xffffffffu, x, s);
+    const bool hi = (lane & s) != 0;
+    const uint32_t t = __funnelshift_l(y, y, hi ? 32 - s : s);  // rotl: lanes with bit s move bits down
+    const uint32_t keep = hi ? ~m0 : m0;
+    x = (x & keep) | (t & ~keep);
+  }
+  return x;
+}
+
+template <int NSTAGES>
+__global__ void __launch_bounds__(kSplitThreads)
+tdes_split_kernel(const uint2* in, uint2* out, size_t nblocks,
+                  const __grid_constant__ RoundMasks<16 * NSTAGES> mk, uint32_t c) {
+  __shared__ uint32_t st[64 * kStride];
+  const unsigned lane = threadIdx.x & 31u;
+  const int g = threadIdx.x >> 5;  // this warp's S-box
+  int win[2][6], own[2][4];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+#pragma unroll
+    for (int i = 0; i < 6; ++i) win[h][i] = tdes_gen::kWin[h][g][i] * kStride + lane;
+#pragma unroll
+    for (int o = 0; o < 4; ++o) own[h][o] = tdes_gen::kOwn[h][g][o] * kStride + lane;
+  }
+  const size_t ntiles = (nblocks + kTileBlocks - 1) / kTileBlocks;
+  for (size_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const size_t base = tile * kTileBlocks;
+    // load: warp g takes groups 4g..4g+3 (32 consecutive blocks each)
+#pragma unroll
+    for (int qq = 0; qq < 4; ++qq) {
+      const int q = 4 * g + qq;
+      const size_t b = base + 32 * q + lane;
+      const uint2 v = b < nblocks ? __ldcs(in + b) : make_uint2(0u, 0u);
+      st[lane * kStride + q] = warp_transpose32(v.x, lane);         // plane `lane` of group q
+      st[(32 + lane) * kStride + q] = warp_transpose32(v.y, lane);
+    }
+    __syncthreads();
+    uint32_t H[2][4];  // the planes of half A (0) and B (1) this warp's S-box writes
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int o = 0; o < 4; ++o) H[h][o] = st[own[h][o]];
+    // 16*NSTAGES rounds; stage s round rr updates A iff (rr + s) is even
+#pragma unroll 1
+    for (int r = 0; r < 16 * NSTAGES; ++r) {
+      const int upd = (((r & 15) + (r >> 4)) & 1);  // 0: update A from B, 1: update B from A
+      const uint32_t* S = mk.s[r] + 6 * g;
+      uint32_t x[6];
+      if (upd == 0) {  // warp-uniform branch; keeps the index arrays in registers
+#pragma unroll
+        for (int i = 0; i < 6; ++i) x[i] = tdes_gen::kxor<true>(st[win[1][i]], S[i], 0u, c);
+        tdes_gen::sbox_by_index(g, x[0], x[1], x[2], x[3], x[4], x[5], H[0][0], H[0][1], H[0][2], H[0][3]);
+#pragma unroll
+        for (int o = 0; o < 4; ++o) st[own[0][o]] = H[0][o];
+      } else {
+#pragma unroll
+        for (int i = 0; i < 6; ++i) x[i] = tdes_gen::kxor<true>(st[win[0][i]], S[i], 0u, c);
+        tdes_gen::sbox_by_index(g, x[0], x[1], x[2], x[3], x[4], x[5], H[1][0], H[1][1], H[1][2], H[1][3]);
+#pragma unroll
+        for (int o = 0; o < 4; ++o) st[own[1][o]] = H[1][o];
+      }
+      __syncthreads();
+    }
+    // FP (renaming) + store: warp g writes groups 4g..4g+3
+#pragma unroll
+    for (int qq = 0; qq < 4; ++qq) {
+      const int q = 4 * g + qq;
+      const uint32_t wx = warp_transpose32(st[tdes_gen::kOutSrc[lane] * kStride + q], lane);
+      const uint32_t wy = warp_transpose32(st[tdes_gen::kOutSrc[32 + lane] * kStride + q], lane);
+      const size_t b = base + 32 * q + lane;
+      if (b < nblocks) __stcs(out + b, make_uint2(wx, wy));
+    }
+    __syncthreads();
+  }
+}
+
 // ------------------------------------------------------------ launching ---
 
 constexpr int kMaxDevices = 64;
@@ -269,9 +372,14 @@ int check_buffers(const void* in, const void* out, size_t nblocks) {
   return TDES_OK;
 }
 
+// Auto mode: the split (latency) kernel for launches of at most this many
+// 1024-block tiles, the throughput kernel above (measured crossover).
+constexpr size_t kSplitMaxTiles = 296;
+
+// mode: 0 auto, 1 throughput kernel, 2 split (latency) kernel.
 template <int NSTAGES>
 int launch(const uint32_t (*masks)[48], const void* in, void* out, size_t nblocks,
-           cudaStream_t stream) {
+           cudaStream_t stream, int mode = 0) {
   if (nblocks == 0) return TDES_OK;
   const int rc = check_buffers(in, out, nblocks);
   if (rc) return rc;
@@ -288,6 +396,14 @@ int launch(const uint32_t (*masks)[48], const void* in, void* out, size_t nblock
   if (dev < 0 || dev >= kMaxDevices) return TDES_ERR_INVALID_ARG;
   const bool vec4 = (((uintptr_t)in | (uintptr_t)out) & 15u) == 0;
   const size_t ntiles = (nblocks + kTileBlocks - 1) / kTileBlocks;
+  if (mode == 2 || (mode == 0 && ntiles <= kSplitMaxTiles)) {
+    const size_t cap = (size_t)num_sms(dev) * 8u;  // up to 8 teams per SM
+    const unsigned sgrid = (unsigned)(ntiles < cap ? ntiles : cap);
+    tdes_split_kernel<NSTAGES><<<sgrid, kSplitThreads, 0, stream>>>(
+        static_cast<const uint2*>(in), static_cast<uint2*>(out), nblocks, mk, kMulhiC);
+    e = cudaGetLastError();
+    return e == cudaSuccess ? TDES_OK : cuda_fail(e);
+  }
   // one resident CTA per SM; with fewer tiles than SMs, one tile per CTA
   const int occ = vec4 ? occupancy<NSTAGES, true>(dev) : occupancy<NSTAGES, false>(dev);
   const size_t resident = (size_t)num_sms(dev) * (size_t)occ;
@@ -315,6 +431,12 @@ extern "C" int tdes_ecb_decrypt(const tdes_schedule* s, const void* in, void* ou
                                 tdes_stream_t stream) {
   if (!s) return TDES_ERR_INVALID_ARG;
   return launch<3>(s->mask[1], in, out, nblocks, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" int tdes_ecb_crypt_mode(const tdes_schedule* s, int decrypt, const void* in, void* out,
+                                   size_t nblocks, int mode, tdes_stream_t stream) {
+  if (!s || (decrypt != 0 && decrypt != 1) || mode < 0 || mode > 2) return TDES_ERR_INVALID_ARG;
+  return launch<3>(s->mask[decrypt], in, out, nblocks, reinterpret_cast<cudaStream_t>(stream), mode);
 }
 
 extern "C" int des_ecb_encrypt(const des_schedule* s, const void* in, void* out, size_t nblocks,

@@ -257,3 +257,25 @@ def test_paper_design_kernel_vs_oracle(tdes, n):
     assert np.array_equal(c.cpu().numpy(), oracle.tdes_ecb(*ks, p))
     d = base.run(c, decrypt=True)
     assert np.array_equal(d.cpu().numpy(), p)
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("n", [1, 31, 32, 33, 1023, 1024, 1025, 5000, 131072, 300000])
+@pytest.mark.parametrize("decrypt", [False, True])
+def test_kernel_modes_vs_oracle(tdes, mode, n, decrypt):
+    """Throughput kernel (mode 1) and S-box-split latency kernel (mode 2), forced."""
+    keys = synthetic.KEYS_3KEY if n % 2 else synthetic.KEYS_2KEY
+    p = synthetic.plaintext_bytes(3 * n + mode, n)
+    s = tdes.key_schedule(*keys)
+    got = tdes.ecb_crypt_mode(to_dev(p), s, mode, decrypt=decrypt).cpu().numpy()
+    assert np.array_equal(got, oracle.tdes_ecb(*keys, p, decrypt=decrypt))
+
+
+def test_split_mode_in_place_and_many_tiles(tdes):
+    n = 8 * 148 * 1024 + 77          # more tiles than the split grid: tile loop
+    s = tdes.key_schedule(*synthetic.KEYS_3KEY)
+    x = torch.empty(8 * n, dtype=torch.uint8, device="cuda")
+    tdes.fill_splitmix64(x)
+    ref = tdes.ecb_crypt_mode(x, s, 1)
+    tdes.ecb_crypt_mode(x, s, 2, out=x)
+    assert torch.equal(x, ref)

@@ -284,6 +284,43 @@ def emit_round(half):
     return "\n".join(lines)
 
 
+def split_tables():
+    """Per-S-box plane indices for the S-box-split latency kernel.
+
+    win[h][g][i]: plane of E-window input i of S-box g when the round reads half h
+    (0 = A, 1 = B); own[h][g][o]: plane of half h that receives output o of S-box g.
+    """
+    halves = (A_IDX, B_IDX)
+    pinv = [None] * 32
+    for i, m in enumerate(P_SRC):
+        pinv[m] = i
+    win = [[[halves[h][T.E[6 * g + i] - 1] for i in range(6)] for g in range(8)] for h in range(2)]
+    own = [[[halves[h][pinv[4 * g + o]] for o in range(4)] for g in range(8)] for h in range(2)]
+    return win, own
+
+
+def emit_split_tables():
+    win, own = split_tables()
+
+    def arr(name, vals):
+        return f"__device__ const uint8_t {name} = {{{', '.join(map(str, vals))}}};"
+    h = ["// ---- S-box-split latency mode (one warp per S-box; csrc/tdes_kernel.cu) ----",
+         "// kWin[h][g][i]: plane of E-window input i of S-box g read from half h (0 = A, 1 = B);",
+         "// kOwn[h][g][o]: plane of half h receiving output o of S-box g; kOutSrc = output_planes.",
+         arr("kWin[2][8][6]", [v for hh in win for g in hh for v in g]),
+         arr("kOwn[2][8][4]", [v for hh in own for g in hh for v in g]),
+         arr("kOutSrc[64]", OUT_SRC),
+         "",
+         "// S-box g (warp-uniform) applied to inputs x, XOR/fused into d0..d3.",
+         "__device__ __forceinline__ void sbox_by_index(int g, uint32_t x0, uint32_t x1, uint32_t x2,",
+         "    uint32_t x3, uint32_t x4, uint32_t x5, uint32_t& d0, uint32_t& d1, uint32_t& d2, uint32_t& d3) {",
+         "  switch (g) {"]
+    for g in range(8):
+        h.append(f"    case {g}: sbox{g + 1}(x0, x1, x2, x3, x4, x5, d0, d1, d2, d3); break;")
+    h += ["    default: break;", "  }", "}", ""]
+    return h
+
+
 def emit_header(circs):
     T.check()
     total = sum(len(c["gates"]) for c in circs)
@@ -351,6 +388,7 @@ def emit_header(circs):
         h.append(f"  Q[{k}] = P[{OUT_SRC[k]}];")
     h.append("}")
     h.append("")
+    h += emit_split_tables()
     h.append("}  // namespace tdes_gen")
     h.append("")
     return "\n".join(h)
