@@ -425,7 +425,140 @@ static void prune(Result *r) {
   r->cost = s->n - 6;
 }
 
+/* Local search step: drop the gates used only by 1-2 randomly chosen outputs
+ * and rebuild those outputs against everything that remains. */
+static void improve_trial(const Result *start, const tt_t targets[4], const Cfg *cfg,
+                          uint64_t seed, Result *res) {
+  uint64_t rng = seed;
+  memcpy(res, start, sizeof(Result));
+  int order[4] = {0, 1, 2, 3};
+  for (int k = 3; k > 0; k--) {
+    const int j = (int)(rnd(&rng) % (uint64_t)(k + 1));
+    const int t = order[k];
+    order[k] = order[j];
+    order[j] = t;
+  }
+  const int nsel = 1 + (int)(rnd(&rng) % 2);
+  for (int q = 0; q < nsel; q++) {
+    res->fh[order[q]] = -1;
+    res->out[order[q]] = 0; /* placeholder: input x0 keeps nothing alive */
+  }
+  prune(res);
+  St *s = &res->s;
+  for (int q = 0; q < nsel; q++) {
+    const int o = order[q];
+    if (cfg->fuse) {
+      OutChoice oc;
+      if (create_output(s, targets[o], cfg, &rng, &oc) < 0) {
+        res->cost = 1 << 20;
+        return;
+      }
+      if (oc.plain) res->out[o] = oc.g, res->neg[o] = oc.neg, res->fh[o] = -1;
+      else res->fu[o] = oc.u, res->fv[o] = oc.v, res->fh[o] = oc.h, res->out[o] = -1;
+    } else {
+      int ng = 0;
+      const int g = create(s, targets[o], ~0ull, 0, 0, cfg, &rng, &ng);
+      if (g < 0) {
+        res->cost = 1 << 20;
+        return;
+      }
+      res->out[o] = g, res->neg[o] = ng, res->fh[o] = -1;
+    }
+  }
+  prune(res);
+}
+
+static int read_circuit(Result *r) {
+  St *s = &r->s;
+  memset(r, 0, sizeof *r);
+  for (int i = 0; i < 6; i++) s->tt[i] = VARS[i];
+  s->n = 6;
+  int n;
+  if (scanf("%d", &n) != 1) return -1;
+  for (int k = 0; k < n; k++) {
+    int lut, a, b, c;
+    if (scanf("%d %d %d %d", &lut, &a, &b, &c) != 4) return -1;
+    add_gate(s, lut, a, b, c);
+  }
+  for (int o = 0; o < 4; o++) {
+    int fused, a, b, c;
+    if (scanf("%d %d %d %d", &fused, &a, &b, &c) != 4) return -1;
+    if (fused) r->fu[o] = a, r->fv[o] = b, r->fh[o] = c, r->out[o] = -1;
+    else r->out[o] = a, r->neg[o] = b, r->fh[o] = -1;
+  }
+  prune(r);
+  return 0;
+}
+
+static void print_result(const Result *b) {
+  printf("{\"gates\": [");
+  for (int g = 6; g < b->s.n; g++)
+    printf("%s[%d, %d, %d, %d]", g > 6 ? ", " : "", b->s.lut[g], b->s.in[g][0], b->s.in[g][1],
+           b->s.in[g][2]);
+  printf("], \"outputs\": [%d, %d, %d, %d], \"neg\": [%d, %d, %d, %d], \"fuse\": [", b->out[0],
+         b->out[1], b->out[2], b->out[3], b->neg[0], b->neg[1], b->neg[2], b->neg[3]);
+  for (int o = 0; o < 4; o++) {
+    if (b->fh[o] >= 0) printf("%s[%d, %d, %d]", o ? ", " : "", b->fu[o], b->fv[o], b->fh[o]);
+    else printf("%snull", o ? ", " : "");
+  }
+  printf("], \"cost\": %d}\n", b->cost);
+}
+
+/* improve mode: hill climbing with parallel restarts from the best circuit so
+ * far; equal-cost moves are accepted so the walk can cross plateaus. */
+static int improve_main(int argc, char **argv) {
+  if (argc != 10) {
+    fprintf(stderr, "usage: %s improve rounds trials seed levels t0 t1 t2 t3 < circuit\n", argv[0]);
+    return 2;
+  }
+  const int rounds = atoi(argv[2]);
+  const long trials = atol(argv[3]);
+  const uint64_t seed = strtoull(argv[4], 0, 10);
+  const int lv = atoi(argv[5]);
+  Cfg cfg = {lv % 10, (lv / 10) % 10 >= 1, lv >= 100};
+  tt_t targets[4];
+  for (int o = 0; o < 4; o++) targets[o] = strtoull(argv[6 + o], 0, 16);
+  Result cur;
+  if (read_circuit(&cur) < 0) {
+    fprintf(stderr, "bad circuit on stdin\n");
+    return 2;
+  }
+  Result best = cur;
+  for (int it = 0; it < rounds; it++) {
+    Result rb;
+    rb.cost = 1 << 20;
+#pragma omp parallel
+    {
+      Result *r = (Result *)malloc(sizeof(Result));
+#pragma omp for schedule(dynamic, 1)
+      for (long t = 0; t < trials; t++) {
+        improve_trial(&cur, targets, &cfg, seed * 7777777ull + (uint64_t)it * 1000003ull + (uint64_t)t, r);
+#pragma omp critical
+        {
+          if (r->cost < rb.cost) memcpy(&rb, r, sizeof(Result));
+        }
+      }
+      free(r);
+    }
+    if (rb.cost <= cur.cost) cur = rb;
+    if (cur.cost < best.cost) {
+      best = cur;
+      fprintf(stderr, "round %d: cost %d\n", it, best.cost);
+    }
+  }
+  print_result(&best);
+  return 0;
+}
+
 int main(int argc, char **argv) {
+  if (argc > 1 && strcmp(argv[1], "improve") == 0) {
+    for (int i = 0; i < 6; i++) {
+      VARS[i] = 0;
+      for (int v = 0; v < 64; v++)
+        if ((v >> (5 - i)) & 1) VARS[i] |= 1ull << v;
+    }
+    return improve_main(argc, argv);
+  }
   if (argc != 8) {
     fprintf(stderr, "usage: %s trials seed full_levels t0 t1 t2 t3\n", argv[0]);
     return 2;
