@@ -309,7 +309,7 @@ def run_ours(args, rank, world, local_rank):
     del x
     torch.cuda.empty_cache()
     hout = torch.empty_like(hin).pin_memory()
-    pipe = tdes.HostPipeline(chunk_blocks=1 << 21, nstreams=4, device=dev)
+    pipe = tdes.HostPipeline(chunk_blocks=1 << 22, nstreams=3, device=dev)  # tools/e2e_sweep.py
     e2e_steps = max(1, min(args.steps, 10))
     pipe.run(sched, hin, hout)      # warmup
     torch.cuda.synchronize()
@@ -362,7 +362,7 @@ def run_ours(args, rank, world, local_rank):
             "clocks": clocks,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * n,
                     "d2h_bytes_per_step": 8 * n,
-                    "how": "tdes_ecb_crypt_host: pinned host in/out, 32 MiB chunks on 4 streams (H2D, kernel, D2H overlapped)",
+                    "how": "tdes_ecb_crypt_host: pinned host in/out, 32 MiB chunks on 3 streams (H2D, kernel, D2H overlapped)",
                     "steps": e2e_steps},
             "gpu_launches": args.steps,
             "check": {"device_roundtrip_mismatch_blocks": mismatch, "ciphertext_sum64": f"{digest:016x}"},
