@@ -25,7 +25,7 @@
  * value, truth-table bit v has x_i = bit (5-i) of v); signal 6+k is gate k.
  *
  * Usage: sbox_search <trials> <seed> <levels> <t0> <t1> <t2> <t3>
- *        levels = full_levels + 10 * all_forms + 100 * fuse
+ *        levels = full_levels + 10 * all_forms + 100 * fuse + 1000 * double_levels
  *        (all_forms: try AND/OR join forms too; fuse: fold the Feistel XOR into
  *        2-input output joins, minimizing gates + unfused outputs)
  *        (t_o = 64-bit truth table of output bit o, hex)
@@ -121,10 +121,58 @@ static int find_single(St *s, tt_t T, tt_t M, uint64_t *rng) {
   return -1;
 }
 
+/* two new gates: T = LUT(a, b, g), g = LUT(c, d, e), a..e existing.  For each
+ * pair (a, b) the regions where T is not constant fix g up to a per-region
+ * polarity; a triple scan then looks for g.  Expensive (O(n^5) worst case):
+ * used only at the top recursion levels (Cfg.double_levels). */
+static int find_double(St *s, tt_t T, tt_t M, uint64_t *rng) {
+  const int n = s->n;
+  if (n + 2 > MAXG) return -1;
+  const int off = n ? (int)(rnd(rng) % (uint64_t)n) : 0;
+  for (int ia = 0; ia < n; ia++) {
+    const int a = (ia + off) % n;
+    const tt_t A = s->tt[a];
+    for (int b = 0; b < n; b++) {
+      if (b == a) continue;
+      const tt_t B = s->tt[b];
+      const tt_t R[4] = {M & ~A & ~B, M & ~A & B, M & A & ~B, M & A & B};
+      int mixed[4], k = 0;
+      tt_t U = 0;
+      for (int q = 0; q < 4; q++) {
+        const tt_t t = T & R[q];
+        if (t && t != R[q]) mixed[k++] = q, U |= R[q];
+      }
+      if (k == 0) continue;
+      for (int pol = 0; pol < (1 << (k - 1)); pol++) {
+        tt_t flip = 0;
+        for (int j = 1; j < k; j++)
+          if ((pol >> (j - 1)) & 1) flip |= R[mixed[j]];
+        const tt_t Tg = T ^ flip;
+        for (int c = 0; c < n; c++) {
+          const tt_t C = s->tt[c];
+          for (int d = c + 1; d < n; d++) {
+            const tt_t D = s->tt[d];
+            for (int e = d + 1; e < n; e++) {
+              const int lut = fit3(C, D, s->tt[e], Tg, U);
+              if (lut < 0) continue;
+              const int g = add_gate(s, lut, c, d, e);
+              const int out = fit3(A, B, s->tt[g], T, M);
+              if (out >= 0) return add_gate(s, out, a, b, g);
+              s->n--; /* cannot happen; undo */
+            }
+          }
+        }
+      }
+    }
+  }
+  return -1;
+}
+
 typedef struct {
   int full_levels;
   int all_forms;
   int fuse;
+  int double_levels;
 } Cfg;
 
 static int create(St *s, tt_t T, tt_t M, int selused, int level, const Cfg *cfg, uint64_t *rng,
@@ -180,6 +228,13 @@ static int create(St *s, tt_t T, tt_t M, int selused, int level, const Cfg *cfg,
   if (g >= 0) {
     *neg = 0;
     return g;
+  }
+  if (level < cfg->double_levels) {
+    g = find_double(s, T, M, rng);
+    if (g >= 0) {
+      *neg = 0;
+      return g;
+    }
   }
   int cand[6], nc = 0;
   for (int i = 0; i < 6; i++)
@@ -515,7 +570,7 @@ static int improve_main(int argc, char **argv) {
   const long trials = atol(argv[3]);
   const uint64_t seed = strtoull(argv[4], 0, 10);
   const int lv = atoi(argv[5]);
-  Cfg cfg = {lv % 10, (lv / 10) % 10 >= 1, lv >= 100};
+  Cfg cfg = {lv % 10, (lv / 10) % 10 >= 1, (lv / 100) % 10 >= 1, lv / 1000};
   tt_t targets[4];
   for (int o = 0; o < 4; o++) targets[o] = strtoull(argv[6 + o], 0, 16);
   Result cur;
@@ -566,7 +621,7 @@ int main(int argc, char **argv) {
   const long trials = atol(argv[1]);
   const uint64_t seed = strtoull(argv[2], 0, 10);
   const int lv = atoi(argv[3]);
-  Cfg cfg = {lv % 10, (lv / 10) % 10 >= 1, lv >= 100};
+  Cfg cfg = {lv % 10, (lv / 10) % 10 >= 1, (lv / 100) % 10 >= 1, lv / 1000};
   tt_t targets[4];
   for (int o = 0; o < 4; o++) targets[o] = strtoull(argv[4 + o], 0, 16);
   for (int i = 0; i < 6; i++) {
