@@ -57,6 +57,13 @@ struct RoundMasks {
   uint32_t k[NROUNDS][48];  // read only by the MULHI = false key XOR
 };
 
+// The split (latency) kernel rebuilds k from s, so it takes half the parameter
+// block: launch cost grows with the parameter size (tools/exp/param_lat.cu).
+template <int NROUNDS>
+struct RoundS {
+  uint32_t s[NROUNDS][48];
+};
+
 // Key-XOR form per variant (tdes_gen::kxor): measured on B200, the loaded-k
 // form is 9% faster for 3DES; for single DES ptxas emits 32-bit per-thread
 // loads for k that saturate the ADU pipe, and rebuilding k from s is 1.9x faster.
@@ -269,7 +276,7 @@ __device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, unsigned lane) 
 template <int NSTAGES>
 __global__ void __launch_bounds__(kSplitThreads)
 tdes_split_kernel(const uint2* in, uint2* out, size_t nblocks,
-                  const __grid_constant__ RoundMasks<16 * NSTAGES> mk, uint32_t c) {
+                  const __grid_constant__ RoundS<16 * NSTAGES> mk, uint32_t c) {
   __shared__ uint32_t st[64 * kStride];
   const unsigned lane = threadIdx.x & 31u;
   const int g = threadIdx.x >> 5;  // this warp's S-box
@@ -402,8 +409,10 @@ int launch(const uint32_t (*masks)[48], const void* in, void* out, size_t nblock
   if (mode == 2 || (mode == 0 && ntiles <= kSplitMaxTiles)) {
     const size_t cap = (size_t)num_sms(dev) * 8u;  // up to 8 teams per SM
     const unsigned sgrid = (unsigned)(ntiles < cap ? ntiles : cap);
+    RoundS<16 * NSTAGES> ms;
+    memcpy(ms.s, mk.s, sizeof ms.s);
     tdes_split_kernel<NSTAGES><<<sgrid, kSplitThreads, 0, stream>>>(
-        static_cast<const uint2*>(in), static_cast<uint2*>(out), nblocks, mk, kMulhiC);
+        static_cast<const uint2*>(in), static_cast<uint2*>(out), nblocks, ms, kMulhiC);
     e = cudaGetLastError();
     return e == cudaSuccess ? TDES_OK : cuda_fail(e);
   }
