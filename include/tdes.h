@@ -112,9 +112,12 @@ int des_ecb_decrypt(const des_schedule *s, const void *in, void *out, size_t nbl
  * one chunk overlap the kernel of another.  Blocks until the result is in
  * host_out (it synchronizes the given streams).
  *   host_in/host_out  host buffers (pinned for copy/compute overlap); may alias.
- *   workspace         device buffer of >= nstreams * chunk_blocks * 8 bytes.
+ *   workspace         device buffer of >= nstreams * chunk_blocks * 8 bytes,
+ *                     16-byte aligned (the chunks then take the 128-bit path).
+ *   chunk_blocks      blocks per chunk, even (> 0).
  *   decrypt           0 = encrypt, 1 = decrypt.
- * Errors: TDES_ERR_INVALID_ARG, TDES_ERR_WORKSPACE, TDES_ERR_CUDA.
+ * Errors: TDES_ERR_INVALID_ARG, TDES_ERR_MISALIGNED (workspace not 16-byte
+ * aligned or chunk_blocks odd), TDES_ERR_WORKSPACE, TDES_ERR_CUDA.
  */
 int tdes_ecb_crypt_host(const tdes_schedule *s, int decrypt, const void *host_in, void *host_out,
                         size_t nblocks, void *workspace, size_t workspace_bytes,
