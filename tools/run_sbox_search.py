@@ -51,7 +51,11 @@ def main():
     ap.add_argument("--levels", type=int, default=2)
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--boxes", default="1,2,3,4,5,6,7,8")
+    ap.add_argument("--out", default=None, help="circuit file to update (default tools/circuits/lut3_search.json)")
     a = ap.parse_args()
+    global OUT
+    if a.out:
+        OUT = a.out
     build()
     best = load()
     for g in [int(x) - 1 for x in a.boxes.split(",")]:
