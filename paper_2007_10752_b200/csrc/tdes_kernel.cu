@@ -57,11 +57,12 @@ struct RoundMasks {
   uint32_t k[NROUNDS][48];  // read only by the MULHI = false key XOR
 };
 
-// The split (latency) kernel rebuilds k from s, so it takes half the parameter
-// block: launch cost grows with the parameter size (tools/exp/param_lat.cu).
+// The split (latency) kernel takes the subkeys bit-packed (one 48-bit word per
+// round, 384 B for 3DES) and derives s per key bit itself: it is latency bound,
+// and launch cost grows with the parameter size (tools/exp/param_lat.cu).
 template <int NROUNDS>
-struct RoundS {
-  uint32_t s[NROUNDS][48];
+struct RoundKeys {
+  uint64_t k[NROUNDS];  // bit 47 - b = subkey bit b (E position b), consumption order
 };
 
 // Key-XOR form per variant (tdes_gen::kxor): measured on B200, the loaded-k
@@ -276,7 +277,7 @@ __device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, unsigned lane) 
 template <int NSTAGES>
 __global__ void __launch_bounds__(kSplitThreads)
 tdes_split_kernel(const uint2* in, uint2* out, size_t nblocks,
-                  const __grid_constant__ RoundS<16 * NSTAGES> mk, uint32_t c) {
+                  const __grid_constant__ RoundKeys<16 * NSTAGES> mk, uint32_t c) {
   __shared__ uint32_t st[64 * kStride];
   const unsigned lane = threadIdx.x & 31u;
   const int g = threadIdx.x >> 5;  // this warp's S-box
@@ -310,7 +311,11 @@ tdes_split_kernel(const uint2* in, uint2* out, size_t nblocks,
 #pragma unroll 1
     for (int r = 0; r < 16 * NSTAGES; ++r) {
       const int upd = (((r & 15) + (r >> 4)) & 1);  // 0: update A from B, 1: update B from A
-      const uint32_t* S = mk.s[r] + 6 * g;
+      // this S-box's 6 subkey bits (bit 47 - b of the packed subkey = E position b)
+      const uint32_t kb = (uint32_t)(mk.k[r] >> (42 - 6 * g)) & 63u;
+      uint32_t S[6];
+#pragma unroll
+      for (int i = 0; i < 6; ++i) S[i] = 1u - (((kb >> (5 - i)) & 1u) << 1);  // s = k | 1 = +1 / -1
       uint32_t x[6];
       if (upd == 0) {  // warp-uniform branch; keeps the index arrays in registers
 #pragma unroll
@@ -409,8 +414,12 @@ int launch(const uint32_t (*masks)[48], const void* in, void* out, size_t nblock
   if (mode == 2 || (mode == 0 && ntiles <= kSplitMaxTiles)) {
     const size_t cap = (size_t)num_sms(dev) * 8u;  // up to 8 teams per SM
     const unsigned sgrid = (unsigned)(ntiles < cap ? ntiles : cap);
-    RoundS<16 * NSTAGES> ms;
-    memcpy(ms.s, mk.s, sizeof ms.s);
+    RoundKeys<16 * NSTAGES> ms;
+    for (int r = 0; r < 16 * NSTAGES; ++r) {
+      uint64_t w = 0;
+      for (int b = 0; b < 48; ++b) w = (w << 1) | (masks[r][b] ? 1u : 0u);
+      ms.k[r] = w;
+    }
     tdes_split_kernel<NSTAGES><<<sgrid, kSplitThreads, 0, stream>>>(
         static_cast<const uint2*>(in), static_cast<uint2*>(out), nblocks, ms, kMulhiC);
     e = cudaGetLastError();

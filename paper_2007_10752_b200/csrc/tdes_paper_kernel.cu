@@ -20,16 +20,15 @@
 #include <stdint.h>
 
 #include "../../include/tdes_paper.h"
-#include "gen/tdes_host_tables.h"
 
 namespace {
 
 thread_local int g_err = 0;
 
-// Tables for the device, from the generated product tables (tools/des_tables.py).
+// Tables for the device, from the generated product tables (tools/des_tables.py);
+// c_shifts is statically initialised at module load, so calls never write shared state.
 #include "gen/tdes_paper_tables.cuh"
 
-__constant__ int c_shifts[16];
 
 __global__ void __launch_bounds__(64) paper_keygen_kernel(const uint8_t* keys /*3x8*/,
                                                           uint8_t* subkeys /*3x16x48*/) {
@@ -112,10 +111,6 @@ extern "C" int tdes_paper_ecb(const uint8_t* dev_keys, const void* in, void* out
   if (!in || !out) return TDES_ERR_INVALID_ARG;
   if (nblocks > 0x7FFFFFFFu) return TDES_ERR_INVALID_ARG;  // one CTA per block (grid.x limit)
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  int sh[16];
-  for (int i = 0; i < 16; ++i) sh[i] = kShifts[i];
-  cudaError_t e = cudaMemcpyToSymbolAsync(c_shifts, sh, sizeof sh, 0, cudaMemcpyHostToDevice, st);
-  if (e != cudaSuccess) return fail(e);
   uint8_t* sk = static_cast<uint8_t*>(workspace);
   paper_keygen_kernel<<<3, 64, 0, st>>>(dev_keys, sk);
   const uint8_t* K[3] = {sk, sk + 16 * 48, sk + 2 * 16 * 48};
@@ -129,6 +124,6 @@ extern "C" int tdes_paper_ecb(const uint8_t* dev_keys, const void* in, void* out
                                                    : static_cast<const uint8_t*>(out),
                                             static_cast<uint8_t*>(out), K[order[s]], dir);
   }
-  e = cudaGetLastError();
+  const cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? TDES_OK : fail(e);
 }

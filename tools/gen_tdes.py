@@ -423,7 +423,9 @@ def emit_paper_tables():
         "// Appendix A tables (PAPER.md:208-353), 1-based, for the read-only path (P:128).",
         "#pragma once",
         arr("d_pc1", T.PC1), arr("d_pc2", T.PC2), arr("d_ip", T.IP), arr("d_e", T.E),
-        arr("d_sbox", sbox), arr("d_p", T.P), arr("d_fp", T.FP), "",
+        arr("d_sbox", sbox), arr("d_p", T.P), arr("d_fp", T.FP),
+        "// shift_keys in constant memory: every thread reads the same entry (P:128)",
+        f"__constant__ int c_shifts[16] = {{{', '.join(map(str, T.SHIFTS))}}};", "",
     ])
 
 

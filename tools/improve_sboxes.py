@@ -39,9 +39,13 @@ def main():
     ap.add_argument("--levels", type=int, default=112)
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--boxes", default="1,2,3,4,5,6,7,8")
+    ap.add_argument("--out", default=None, help="circuit file to update (default tools/circuits/lut3_search.json)")
     a = ap.parse_args()
     rs.build()
-    best = rs.load()
+    # start from the best verified circuit per S-box over every file in tools/circuits/
+    best = {g: dict(c, sbox=g) for g, c in gen_tdes.load_searched().items()}
+    if a.out:
+        rs.OUT = a.out
     for g in [int(x) - 1 for x in a.boxes.split(",")]:
         start = best[g]
         targets = [f"{gen_tdes.sbox_tt(g, o):016x}" for o in range(4)]
