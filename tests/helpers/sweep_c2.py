@@ -1,0 +1,107 @@
+"""TEST INFRASTRUCTURE (calls oracle/). BASELINE.json config 2: paper-style size sweep 1 MiB .. 1 GiB, 3DES-ECB encrypt and
+decrypt on one B200, with the CPU oracle timed beside it on the host cores.  Writes a
+markdown table (default profiles/sweep_c2.md).
+
+Per size: device time of one launch (median of 10, CUDA events, data resident), GB/s;
+bit-exactness vs the oracle (every block up to 2^20 blocks, 4096 sampled blocks plus
+the first/last 1024 above that) for both directions; the oracle's wall time on the
+host cores (full size while the estimate stays under the cap, else a timed sample
+scaled up, marked "~").  Config 3 (1-key and 2-key on 256 MiB) rides along.
+"""
+import argparse
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import oracle  # noqa: E402  (test infrastructure: the timed CPU baseline)
+import paper_2007_10752_b200 as tdes  # noqa: E402
+import synthetic  # noqa: E402
+
+
+def dev_time(fn, reps=10):
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        b.synchronize()
+        ts.append(a.elapsed_time(b))
+    return sorted(ts)[len(ts) // 2]
+
+
+def check(keys, x, y, decrypt, n):
+    if n <= 1 << 20:
+        exp = oracle.tdes_ecb(*keys, synthetic.plaintext_bytes(0, n), decrypt=decrypt)
+        return np.array_equal(y.cpu().numpy(), exp), n
+    rng = np.random.default_rng(n + decrypt)
+    idx = np.unique(np.concatenate([rng.integers(0, n, 4096), np.arange(1024), np.arange(n - 1024, n)]))
+    got = y.view(-1, 8)[torch.from_numpy(idx).cuda()].cpu().numpy().reshape(-1)
+    exp = oracle.tdes_ecb(*keys, synthetic.gather_blocks(idx), decrypt=decrypt)
+    return np.array_equal(got, exp), len(idx)
+
+
+def oracle_time(keys, n, cap_s, rate):
+    """Full-size oracle wall time if it fits the cap, else a timed sample scaled up."""
+    est = n / rate if rate else 0
+    m = n if est <= cap_s else max(1 << 16, int(cap_s * rate) // 4)
+    p = synthetic.plaintext_bytes(0, m)
+    out = np.empty_like(p)
+    t0 = time.perf_counter()
+    oracle.tdes_ecb_into(*keys, p, out)
+    dt = time.perf_counter() - t0
+    return dt * n / m, m == n, m / dt
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default="profiles/sweep_c2.md")
+    ap.add_argument("--cap", type=float, default=20.0, help="oracle seconds per point")
+    a = ap.parse_args()
+    N = 1 << 27
+    x = torch.empty(8 * N, dtype=torch.uint8, device="cuda")
+    tdes.fill_splitmix64(x)
+    y = torch.empty_like(x)
+    cores = len(os.sched_getaffinity(0))
+    rate = None
+    lines = ["# Config 2: size sweep, 3DES-EDE ECB on one B200 vs the oracle on host cores", "",
+             f"GPU: {torch.cuda.get_device_name(0)}; host cores used by the oracle: {cores} (OpenMP over blocks).",
+             "Device time = one launch (median of 10, CUDA events, data resident in HBM).",
+             "Oracle = `oracle/tdes_oracle.c` (char per bit, as in the paper), wall clock;",
+             "`~` = extrapolated from a timed sample (the full size would exceed the per-point cap).", "",
+             "| blocks | bytes | op | keys | GPU ms | GPU GB/s | bit-exact (blocks checked) | oracle s | oracle GB/s | GPU/oracle |",
+             "|---|---|---|---|---|---|---|---|---|---|"]
+    points = [(e, op, "3-key") for e in range(17, 28) for op in ("enc", "dec")]
+    points += [(25, op, k) for k in ("1-key", "2-key") for op in ("enc", "dec")]
+    keysets = {"3-key": synthetic.KEYS_3KEY, "2-key": synthetic.KEYS_2KEY, "1-key": synthetic.KEYS_1KEY}
+    for e, op, kname in points:
+        n = 1 << e
+        keys = keysets[kname]
+        s = tdes.key_schedule(*keys)
+        dec = op == "dec"
+        fn = tdes.ecb_decrypt if dec else tdes.ecb_encrypt
+        xs, ys = x[:8 * n], y[:8 * n]
+        ms = dev_time(lambda: fn(xs, s, out=ys))
+        ok, nchk = check(keys, xs, ys, dec, n)
+        osec, full, r = oracle_time(keys, n, a.cap, rate)
+        rate = rate or r
+        gbs = n * 8 / ms / 1e6
+        ogbs = n * 8 / osec / 1e9
+        lines.append(f"| 2^{e} | {n * 8 / 2**20:g} MiB | {op} | {kname} | {ms:.4f} | {gbs:.1f} | "
+                     f"{'yes' if ok else 'NO'} ({nchk}) | {'' if full else '~'}{osec:.2f} | {ogbs:.4f} | "
+                     f"{gbs / ogbs:.0f}x |")
+        print(lines[-1], flush=True)
+    os.makedirs(os.path.dirname(a.out) or ".", exist_ok=True)
+    with open(a.out, "w") as f:
+        f.write("\n".join(lines) + "\n")
+
+
+if __name__ == "__main__":
+    main()
