@@ -9,7 +9,7 @@
 //   S1 load      32 blocks per thread, coalesced (a warp reads 8 KiB contiguous)
 //   S2 transpose two 32x32 bit transposes (PRMT for the 16/8 stages)
 //   S3 IP        register renaming (free)
-//   S4 48 rounds key XOR with lane masks, 8 LOP3 S-box circuits, XOR into the
+//   S4 48 rounds key XOR (one IMAD each, FMA pipe), 8 LOP3 S-box circuits, XOR into the
 //                other half; E and P are operand/destination renaming (free);
 //                the three DES stages are fused, IP/FP between them cancel
 //   S6 FP        register renaming (free)
@@ -172,7 +172,7 @@ __device__ __forceinline__ void crypt_tile(const uint2* in, uint2* out, size_t b
     P[32 + j] = Y[j];
   }
   // ---- S3..S6: IP (renaming), 16*NSTAGES rounds, FP (renaming) ----
-  // One two-round loop body for all stages keeps the 16 warps of the SM inside
+  // One two-round loop body for all stages keeps all warps of the SM inside
   // the instruction cache.  The middle stage starts on the half the first one
   // updated last, so at each stage boundary the halves swap
   // register roles and the same A-then-B body continues.
@@ -215,7 +215,7 @@ __device__ __forceinline__ void crypt_tile(const uint2* in, uint2* out, size_t b
 
 // NSTAGES = 3: fused 3DES (48 rounds); NSTAGES = 1: single DES (16 rounds).
 // Work distribution: CTA c owns the contiguous tile range
-// [ntiles*c/grid, ntiles*(c+1)/grid); its 16 warps claim tiles one at a time
+// [ntiles*c/grid, ntiles*(c+1)/grid); its warps claim tiles one at a time
 // from a shared-memory counter.  Warps of one SM progress at very different
 // rates under the hardware's warp arbitration, so a static per-warp split
 // leaves the SM waiting on its slowest warp (measured: 1.6-2x slower).
