@@ -481,7 +481,7 @@ static void prune(Result *r) {
 }
 
 /* Local search step: drop the gates used only by 1-2 randomly chosen outputs
- * and rebuild those outputs against everything that remains. */
+ * and rebuild those outputs against everything that remains (1-3 outputs). */
 static void improve_trial(const Result *start, const tt_t targets[4], const Cfg *cfg,
                           uint64_t seed, Result *res) {
   uint64_t rng = seed;
@@ -493,7 +493,7 @@ static void improve_trial(const Result *start, const tt_t targets[4], const Cfg 
     order[k] = order[j];
     order[j] = t;
   }
-  const int nsel = 1 + (int)(rnd(&rng) % 2);
+  const int nsel = 1 + (int)(rnd(&rng) % 3); /* rebuild 1-3 of the 4 outputs */
   for (int q = 0; q < nsel; q++) {
     res->fh[order[q]] = -1;
     res->out[order[q]] = 0; /* placeholder: input x0 keeps nothing alive */
