@@ -305,3 +305,14 @@ def test_beyond_2_32_blocks_in_place(tdes):
     assert tdes.count_mismatch(tail, ref) == 0
     del x, tail, ref
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("weak", ["0101010101010101", "FEFEFEFEFEFEFEFE", "E0E0E0E0F1F1F1F1", "1F1F1F1F0E0E0E0E"])
+def test_weak_keys_vs_oracle_and_involution(tdes, weak):
+    """Degenerate keying: with K1=K2=K3 weak, 3DES is DES under a weak key, an involution."""
+    n = 3000
+    p = synthetic.plaintext_bytes(11, n)
+    s = tdes.key_schedule(weak, weak, weak)
+    c = tdes.ecb_encrypt(to_dev(p), s)
+    assert np.array_equal(c.cpu().numpy(), oracle.tdes_ecb(weak, weak, weak, p))
+    assert np.array_equal(tdes.ecb_encrypt(c, s).cpu().numpy(), p)
