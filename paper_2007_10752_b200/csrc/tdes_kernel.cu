@@ -32,14 +32,34 @@ namespace {
 // 12 warps per CTA, one CTA per SM: ptxas then keeps the round in 150 registers
 // without spills (A/B on B200, 1 GiB: 384 threads 42.4, 512 threads 42.1,
 // 448 41.6, 256 37.6 Gblk/s).
-constexpr int kThreads = 384;
+#ifndef TDES_THREADS
+#define TDES_THREADS 384
+#endif
+#ifndef TDES_WORDS
+#define TDES_WORDS 1
+#endif
+constexpr int kThreads = TDES_THREADS;
 constexpr int kMinCtasPerSm = 1;
-constexpr int kBlocksPerThread = 32; // one bit-plane word
-constexpr int kTileBlocks = 32 * kBlocksPerThread;  // per warp: 1024 blocks = 8 KiB
+// Words per bit-plane: a thread holds kWords independent 32-block groups, so
+// each loaded key value and each instruction-issue decision serves kWords words.
+constexpr int kWords = TDES_WORDS;
+constexpr int kGroupBlocks = 32 * 32;  // one 32-block group per lane: 1024 blocks = 8 KiB per warp
+constexpr int kBlocksPerThread = 32 * kWords;
+constexpr int kTileBlocks = kGroupBlocks * kWords;  // per warp
 #ifndef TDES_ROUND_UNROLL
 #define TDES_ROUND_UNROLL 1
 #endif
-constexpr int kRoundUnroll = TDES_ROUND_UNROLL;  // two-round bodies per loop iteration (2 measured 3% slower)
+constexpr int kRoundUnroll = TDES_ROUND_UNROLL;
+// Where the per-thread key operand k of the IMAD key XOR is read from (3DES):
+// 0 = the launch parameters (ptxas emits LDC.64 plus an IMAD.U32 address copy
+//     per load), 1 = a shared-memory copy made at CTA start (one broadcast
+//     LDS.128 per 4 key bits).  s stays a uniform LDCU operand either way.
+// Measured on B200, 1 GiB: 358 -> 370 GB/s for 1; s and k both from shared
+// memory: 348 GB/s.
+#ifndef TDES_KSMEM
+#define TDES_KSMEM 1
+#endif
+constexpr int kKeySmem = TDES_KSMEM;  // two-round bodies per loop iteration (2 measured 3% slower)
 
 thread_local int g_last_cuda_error = 0;
 
@@ -52,7 +72,7 @@ constexpr uint32_t kMulhiC = 0x7FFFFFFFu;
 // s = k | 1 (+1 or -1) where k is the subkey bit's all-ones / all-zeros lane
 // mask; the key XOR is rebuilt from s on the FMA pipe (tdes_gen::kxor).
 template <int NROUNDS>
-struct RoundMasks {
+struct alignas(16) RoundMasks {
   uint32_t s[NROUNDS][48];
   uint32_t k[NROUNDS][48];  // read only by the MULHI = false key XOR
 };
@@ -122,14 +142,27 @@ __device__ __forceinline__ void transpose32(uint32_t (&a)[32]) {
   bitstage<1>(a, 0x55555555u);
 }
 
-// One warp tile: 32 lanes x 32 blocks = 1024 consecutive blocks from `base`.
-// VEC4: in/out 16-byte aligned -> 128-bit accesses (2 blocks per access).
-template <int NSTAGES, bool VEC4>
-__device__ __forceinline__ void crypt_tile(const uint2* in, uint2* out, size_t base, size_t nblocks,
-                                           unsigned lane, const RoundMasks<16 * NSTAGES>& mk,
-                                           uint32_t c) {
-  const bool full = base + kTileBlocks <= nblocks;
-  uint32_t X[32], Y[32];
+// Plane type: one word (uint32_t) or kWords words (tdes_gen::Vec).
+template <int W>
+struct PlaneOf {
+  using type = tdes_gen::Vec<W>;
+};
+template <>
+struct PlaneOf<1> {
+  using type = uint32_t;
+};
+__device__ __forceinline__ uint32_t& word(uint32_t& v, int) { return v; }
+template <int W>
+__device__ __forceinline__ uint32_t& word(tdes_gen::Vec<W>& v, int i) {
+  return v.w[i];
+}
+
+// One 1024-block group (32 lanes x 32 blocks) from `base` into bit-planes X (low
+// words) and Y (high words).  VEC4: in 16-byte aligned -> 128-bit loads.
+template <bool VEC4>
+__device__ __forceinline__ void load_group(const uint2* in, size_t base, size_t nblocks, unsigned lane,
+                                           uint32_t (&X)[32], uint32_t (&Y)[32]) {
+  const bool full = base + kGroupBlocks <= nblocks;
   // ---- S1: load.  Plane bit i <-> the i-th block this lane loads. ----
   if (VEC4) {
     const uint4* in4 = reinterpret_cast<const uint4*>(in + base);
@@ -162,34 +195,15 @@ __device__ __forceinline__ void crypt_tile(const uint2* in, uint2* out, size_t b
       Y[i] = v.y;
     }
   }
-  // ---- S2: to bit-planes ----
   transpose32(X);
   transpose32(Y);
-  uint32_t P[64];
-#pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    P[j] = X[j];
-    P[32 + j] = Y[j];
-  }
-  // ---- S3..S6: IP (renaming), 16*NSTAGES rounds, FP (renaming) ----
-  // One two-round loop body for all stages keeps all warps of the SM inside
-  // the instruction cache.  The middle stage starts on the half the first one
-  // updated last (SURVEY V8), so at each stage boundary the halves swap
-  // register roles and the same A-then-B body continues.
-#pragma unroll kRoundUnroll
-  for (int r = 0; r < 16 * NSTAGES; r += 2) {
-    if (NSTAGES == 3 && (r == 16 || r == 32)) tdes_gen::swap_halves(P);
-    tdes_gen::round_A<kUseMulhi<NSTAGES>>(P, mk.s[r], mk.k[r], c);
-    tdes_gen::round_B<kUseMulhi<NSTAGES>>(P, mk.s[r + 1], mk.k[r + 1], c);
-  }
-  uint32_t Q[64];
-  tdes_gen::output_planes(P, Q);
-#pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    X[j] = Q[j];
-    Y[j] = Q[32 + j];
-  }
-  // ---- S7: back to blocks, store ----
+}
+
+// Inverse of load_group: planes X, Y back to blocks, stored from `base`.
+template <bool VEC4>
+__device__ __forceinline__ void store_group(uint2* out, size_t base, size_t nblocks, unsigned lane,
+                                            uint32_t (&X)[32], uint32_t (&Y)[32]) {
+  const bool full = base + kGroupBlocks <= nblocks;
   transpose32(X);
   transpose32(Y);
   if (VEC4) {
@@ -213,6 +227,56 @@ __device__ __forceinline__ void crypt_tile(const uint2* in, uint2* out, size_t b
   }
 }
 
+// One warp tile: kWords groups of 1024 consecutive blocks from `base`; word w
+// of every plane holds group w.
+template <int NSTAGES, bool VEC4>
+__device__ __forceinline__ void crypt_tile(const uint2* in, uint2* out, size_t base, size_t nblocks,
+                                           unsigned lane, const RoundMasks<16 * NSTAGES>& mk,
+                                           const uint4* ksm, uint32_t c) {
+  using V = typename PlaneOf<kWords>::type;
+  V P[64];
+  // ---- S1 load + S2 transpose to bit-planes ----
+#pragma unroll
+  for (int w = 0; w < kWords; ++w) {
+    uint32_t X[32], Y[32];
+    load_group<VEC4>(in, base + (size_t)w * kGroupBlocks, nblocks, lane, X, Y);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      word(P[j], w) = X[j];
+      word(P[32 + j], w) = Y[j];
+    }
+  }
+  // ---- S3..S6: IP (renaming), 16*NSTAGES rounds, FP (renaming) ----
+  // One two-round loop body for all stages keeps all warps of the SM inside
+  // the instruction cache.  The middle stage starts on the half the first one
+  // updated last (SURVEY V8), so at each stage boundary the halves swap
+  // register roles and the same A-then-B body continues.
+#pragma unroll kRoundUnroll
+  for (int r = 0; r < 16 * NSTAGES; r += 2) {
+    if (NSTAGES == 3 && (r == 16 || r == 32)) tdes_gen::swap_halves(P);
+    if (kKeySmem == 0 || kUseMulhi<NSTAGES>) {
+      tdes_gen::round_A<kUseMulhi<NSTAGES>>(P, mk.s[r], mk.k[r], c);
+      tdes_gen::round_B<kUseMulhi<NSTAGES>>(P, mk.s[r + 1], mk.k[r + 1], c);
+    } else {
+      tdes_gen::round_A<false>(P, mk.s[r], ksm + 12 * r, c);
+      tdes_gen::round_B<false>(P, mk.s[r + 1], ksm + 12 * (r + 1), c);
+    }
+  }
+  V Q[64];
+  tdes_gen::output_planes(P, Q);
+  // ---- S7: back to blocks, store ----
+#pragma unroll
+  for (int w = 0; w < kWords; ++w) {
+    uint32_t X[32], Y[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      X[j] = word(Q[j], w);
+      Y[j] = word(Q[32 + j], w);
+    }
+    store_group<VEC4>(out, base + (size_t)w * kGroupBlocks, nblocks, lane, X, Y);
+  }
+}
+
 // NSTAGES = 3: fused 3DES (48 rounds); NSTAGES = 1: single DES (16 rounds).
 // Work distribution: CTA c owns the contiguous tile range
 // [ntiles*c/grid, ntiles*(c+1)/grid); its warps claim tiles one at a time
@@ -224,18 +288,24 @@ __global__ void __launch_bounds__(kThreads, kMinCtasPerSm)
 tdes_ecb_kernel(const uint2* in, uint2* out, size_t nblocks,
                 const __grid_constant__ RoundMasks<16 * NSTAGES> mk, uint32_t c) {
   __shared__ unsigned int next_tile;
+  constexpr int kKeyVecs = 12 * 16 * NSTAGES;  // 48 key words per round as uint4
+  __shared__ uint4 ksm[kKeySmem == 0 || kUseMulhi<NSTAGES> ? 1 : kKeyVecs];  // k, 9 KiB for 3DES
   const unsigned lane = threadIdx.x & 31u;
   const size_t ntiles = (nblocks + kTileBlocks - 1) / kTileBlocks;
   const size_t lo = ntiles * blockIdx.x / gridDim.x;
   const size_t hi = ntiles * (blockIdx.x + 1) / gridDim.x;
   if (threadIdx.x == 0) next_tile = 0;
+  if (kKeySmem != 0 && !kUseMulhi<NSTAGES>) {
+    const uint4* k4 = reinterpret_cast<const uint4*>(&mk.k[0][0]);
+    for (int i = threadIdx.x; i < kKeyVecs; i += blockDim.x) ksm[i] = k4[i];
+  }
   __syncthreads();
   for (;;) {
     unsigned t = 0;
     if (lane == 0) t = atomicAdd(&next_tile, 1u);
     const size_t tile = lo + __shfl_sync(0xffffffffu, t, 0);
     if (tile >= hi) break;
-    crypt_tile<NSTAGES, VEC4>(in, out, tile * kTileBlocks, nblocks, lane, mk, c);
+    crypt_tile<NSTAGES, VEC4>(in, out, tile * kTileBlocks, nblocks, lane, mk, ksm, c);
   }
 }
 
@@ -289,9 +359,9 @@ tdes_split_kernel(const uint2* in, uint2* out, size_t nblocks,
 #pragma unroll
     for (int o = 0; o < 4; ++o) own[h][o] = tdes_gen::kOwn[h][g][o] * kStride + lane;
   }
-  const size_t ntiles = (nblocks + kTileBlocks - 1) / kTileBlocks;
+  const size_t ntiles = (nblocks + kGroupBlocks - 1) / kGroupBlocks;
   for (size_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const size_t base = tile * kTileBlocks;
+    const size_t base = tile * kGroupBlocks;
     // load: warp g takes groups 4g..4g+3 (32 consecutive blocks each)
 #pragma unroll
     for (int qq = 0; qq < 4; ++qq) {
@@ -410,10 +480,10 @@ int launch(const uint32_t (*masks)[48], const void* in, void* out, size_t nblock
   if (e != cudaSuccess) return cuda_fail(e);
   if (dev < 0 || dev >= kMaxDevices) return TDES_ERR_INVALID_ARG;
   const bool vec4 = (((uintptr_t)in | (uintptr_t)out) & 15u) == 0;
-  const size_t ntiles = (nblocks + kTileBlocks - 1) / kTileBlocks;
-  if (mode == 2 || (mode == 0 && ntiles <= kSplitMaxTiles)) {
+  const size_t ngroups = (nblocks + kGroupBlocks - 1) / kGroupBlocks;
+  if (mode == 2 || (mode == 0 && ngroups <= kSplitMaxTiles)) {
     const size_t cap = (size_t)num_sms(dev) * 8u;  // up to 8 teams per SM
-    const unsigned sgrid = (unsigned)(ntiles < cap ? ntiles : cap);
+    const unsigned sgrid = (unsigned)(ngroups < cap ? ngroups : cap);
     RoundKeys<16 * NSTAGES> ms;
     for (int r = 0; r < 16 * NSTAGES; ++r) {
       uint64_t w = 0;
@@ -426,6 +496,7 @@ int launch(const uint32_t (*masks)[48], const void* in, void* out, size_t nblock
     return e == cudaSuccess ? TDES_OK : cuda_fail(e);
   }
   // one resident CTA per SM; with fewer tiles than SMs, one tile per CTA
+  const size_t ntiles = (nblocks + kTileBlocks - 1) / kTileBlocks;
   const int occ = vec4 ? occupancy<NSTAGES, true>(dev) : occupancy<NSTAGES, false>(dev);
   const size_t resident = (size_t)num_sms(dev) * (size_t)occ;
   const unsigned grid = (unsigned)(ntiles < resident ? ntiles : resident);

@@ -241,14 +241,14 @@ def emit_sbox(g, circ):
     lines = [f"// S{g + 1}: {len(circ['gates'])} lop3 + 4 Feistel XOR ({nf} of them fused with the output's"
              f" final 2-input join) = {circuit_cost(circ)} ALU ops ({circ['source']})",
              "// Inputs x0..x5 = S-box bits b1..b6; each output is XORed into its destination plane.",
-             f"__device__ __forceinline__ void sbox{g + 1}(uint32_t x0, uint32_t x1, uint32_t x2, "
-             "uint32_t x3, uint32_t x4, uint32_t x5,",
-             "    uint32_t& d0, uint32_t& d1, uint32_t& d2, uint32_t& d3) {"]
+             "template <class V>",
+             f"__device__ __forceinline__ void sbox{g + 1}(V x0, V x1, V x2, V x3, V x4, V x5,",
+             "    V& d0, V& d1, V& d2, V& d3) {"]
 
     def name(s):
         return f"x{s}" if s < 6 else f"t{s - 6}"
     for k, (lut, a, b, c) in enumerate(circ["gates"]):
-        lines.append(f"  const uint32_t t{k} = lop3<0x{lut:02x}>({name(a)}, {name(b)}, {name(c)});")
+        lines.append(f"  const V t{k} = lop3<0x{lut:02x}>({name(a)}, {name(b)}, {name(c)});")
     neg = circ.get("neg") or [0, 0, 0, 0]
     for o, s in enumerate(circ["outputs"]):
         f = fuse[o]
@@ -271,11 +271,12 @@ def emit_round(half):
     lines = [f"// One Feistel round updating half {half}: {half} ^= P(S(E(other) ^ K)).",
              "// Key XOR on the FMA pipe (kxor): S = the round's 48 s = k | 1 values, K = the",
              "// masks k (read only when MULHI = false), c = 0x7FFFFFFF.",
-             "template <bool MULHI>",
-             f"__device__ __forceinline__ void round_{half}(uint32_t (&P)[64], const uint32_t* __restrict__ S,",
-             "                                        const uint32_t* __restrict__ K, uint32_t c) {"]
+             "// S and K point to uint32_t or uint4 arrays (kat reads word i of either).",
+             "template <bool MULHI, class V, class SP, class KP>",
+             f"__device__ __forceinline__ void round_{half}(V (&P)[64], const SP* __restrict__ S,",
+             "                                        const KP* __restrict__ K, uint32_t c) {"]
     for g in range(8):
-        xs = [f"kxor<MULHI>(P[{src[T.E[6 * g + i] - 1]}], S[{6 * g + i}], MULHI ? 0u : K[{6 * g + i}], c)"
+        xs = [f"kxor<MULHI>(P[{src[T.E[6 * g + i] - 1]}], kat<{6 * g + i}>(S), MULHI ? 0u : kat<{6 * g + i}>(K), c)"
               for i in range(6)]
         ds = [f"P[{dst[pinv[4 * g + o]]}]" for o in range(4)]
         lines.append(f"  sbox{g + 1}({', '.join(xs)},")
@@ -368,6 +369,59 @@ def emit_header(circs):
         "  return d;",
         "}",
         "",
+        "// Word I of a key-material array of 32-bit words or of 128-bit vectors.",
+        "template <int I>",
+        "__device__ __forceinline__ uint32_t kat(const uint32_t* __restrict__ a) {",
+        "  return a[I];",
+        "}",
+        "template <int I>",
+        "__device__ __forceinline__ uint32_t kat(const uint4* __restrict__ a) {",
+        "  const uint4 v = a[I / 4];",
+        "  return I % 4 == 0 ? v.x : I % 4 == 1 ? v.y : I % 4 == 2 ? v.z : v.w;",
+        "}",
+        "",
+        "// W independent 32-block groups per thread: a plane is W words and every op",
+        "// applies word-wise; one loaded key value serves all W words (the circuits and",
+        "// round functions below are templates on the plane type V = uint32_t or Vec<W>).",
+        "template <int W>",
+        "struct Vec {",
+        "  uint32_t w[W];",
+        "};",
+        "",
+        "template <unsigned LUT, int W>",
+        "__device__ __forceinline__ Vec<W> lop3(const Vec<W>& a, const Vec<W>& b, const Vec<W>& c) {",
+        "  Vec<W> d;",
+        "#pragma unroll",
+        "  for (int i = 0; i < W; ++i) d.w[i] = lop3<LUT>(a.w[i], b.w[i], c.w[i]);",
+        "  return d;",
+        "}",
+        "",
+        "template <int W>",
+        "__device__ __forceinline__ Vec<W>& operator^=(Vec<W>& a, const Vec<W>& b) {",
+        "#pragma unroll",
+        "  for (int i = 0; i < W; ++i) a.w[i] ^= b.w[i];",
+        "  return a;",
+        "}",
+        "",
+        "template <int W>",
+        "__device__ __forceinline__ Vec<W> operator~(const Vec<W>& a) {",
+        "  Vec<W> d;",
+        "#pragma unroll",
+        "  for (int i = 0; i < W; ++i) d.w[i] = ~a.w[i];",
+        "  return d;",
+        "}",
+        "",
+        "template <bool MULHI, int W>",
+        "__device__ __forceinline__ Vec<W> kxor(const Vec<W>& x, uint32_t s, uint32_t kmem, uint32_t c) {",
+        "  uint32_t k = kmem;",
+        "  if (MULHI) asm(\"mul.hi.s32 %0, %1, %2;\" : \"=r\"(k) : \"r\"(c), \"r\"(s));",
+        "  Vec<W> d;",
+        "#pragma unroll",
+        "  for (int i = 0; i < W; ++i)",
+        "    asm(\"mad.lo.u32 %0, %1, %2, %3;\" : \"=r\"(d.w[i]) : \"r\"(x.w[i]), \"r\"(s), \"r\"(k));",
+        "  return d;",
+        "}",
+        "",
     ]
     for g, c in enumerate(circs):
         h.append(emit_sbox(g, c))
@@ -377,13 +431,15 @@ def emit_header(circs):
     h.append(emit_round("B"))
     h.append("")
     h.append("// Exchange the register roles of the halves A (IP left, L0) and B (IP right, R0).")
-    h.append("__device__ __forceinline__ void swap_halves(uint32_t (&P)[64]) {")
+    h.append("template <class V>")
+    h.append("__device__ __forceinline__ void swap_halves(V (&P)[64]) {")
     for a, b in zip(A_IDX, B_IDX):
-        h.append(f"  {{ const uint32_t t = P[{a}]; P[{a}] = P[{b}]; P[{b}] = t; }}")
+        h.append(f"  {{ const V t = P[{a}]; P[{a}] = P[{b}]; P[{b}] = t; }}")
     h.append("}")
     h.append("")
     h.append("// Pre-output (B || A) through FP, renamed into store-transpose order (PAPER.md:74-75).")
-    h.append("__device__ __forceinline__ void output_planes(const uint32_t (&P)[64], uint32_t (&Q)[64]) {")
+    h.append("template <class V>")
+    h.append("__device__ __forceinline__ void output_planes(const V (&P)[64], V (&Q)[64]) {")
     for k in range(64):
         h.append(f"  Q[{k}] = P[{OUT_SRC[k]}];")
     h.append("}")
