@@ -85,11 +85,16 @@ struct RoundKeys {
   uint64_t k[NROUNDS];  // bit 47 - b = subkey bit b (E position b), consumption order
 };
 
-// Key-XOR form per variant (tdes_gen::kxor): measured on B200, the loaded-k
-// form is 9% faster for 3DES; for single DES ptxas emits 32-bit per-thread
-// loads for k that saturate the ADU pipe, and rebuilding k from s is 1.9x faster.
+// Key-XOR form per variant (tdes_gen::kxor).  With k read from the launch
+// parameters, rebuilding k from s (MULHI) was 1.9x faster for single DES (ptxas
+// emitted 32-bit per-thread LDCs that saturated the ADU pipe) and 9% slower for
+// 3DES.  With k from the shared-memory copy (TDES_KSMEM=1) the loaded form wins
+// for both (B200, 1 GiB: DES 828 -> 944 GB/s).
+#ifndef TDES_DES_MULHI
+#define TDES_DES_MULHI 0
+#endif
 template <int NSTAGES>
-constexpr bool kUseMulhi = NSTAGES == 1;
+constexpr bool kUseMulhi = NSTAGES == 1 && (TDES_DES_MULHI || !TDES_KSMEM);
 
 // x >> s as the high word of x * 2^(32-s): IMAD.HI on the FMA pipe instead of
 // SHF on the integer ALU pipe (the kernel's bound).  Left shifts already

@@ -21,7 +21,8 @@ x = torch.empty(8 * n, dtype=torch.uint8, device="cuda"); tdes.fill_splitmix64(x
 y = torch.empty_like(x)
 s = tdes.key_schedule(*synthetic.KEYS_3KEY)
 res = {}
-for name, fn in (("enc", lambda: tdes.ecb_encrypt(x, s, out=y)),):
+ds = tdes.des_key_schedule(synthetic.KEYS_1KEY[0])
+for name, fn in (("enc", lambda: tdes.ecb_encrypt(x, s, out=y)), ("des", lambda: tdes.des_ecb_encrypt(x, ds, out=y))):
     for _ in range(3): fn()
     torch.cuda.synchronize()
     ts = []
@@ -32,7 +33,9 @@ for name, fn in (("enc", lambda: tdes.ecb_encrypt(x, s, out=y)),):
     res[name] = ts[len(ts) // 2]
 tdes.ecb_encrypt(x, s, out=y)
 d = tdes.sum64(y)
-print(f"RESULT enc_ms={res['enc']:.4f} GBps={n*8/res['enc']/1e6:.1f} sum64={d:016x}")
+tdes.des_ecb_encrypt(x, ds, out=y)
+d2 = tdes.sum64(y)
+print(f"RESULT enc_ms={res['enc']:.4f} GBps={n*8/res['enc']/1e6:.1f} sum64={d:016x} des_GBps={n*8/res['des']/1e6:.1f} des_sum64={d2:016x}")
 '''.replace("ROOT", repr(ROOT))
 
 
