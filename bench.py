@@ -42,6 +42,21 @@ WORKLOAD = "3DES-EDE ECB encrypt, 1 GiB (2^27 blocks) per GPU, 3-key (SP 800-67 
 SM_COUNT_NOMINAL = 148
 LOP3_LANES_PER_SM = 64            # B300_MICROARCH.md: LOP3 on the alu pipe, rt_SMSP = 2 -> 16 lanes/clk/SMSP
 HBM_PEAK_FALLBACK = 6650.0        # B200_PROFILING.md fallback (GB/s)
+E2E_MAX_BLOCKS = 1 << 27          # e2e leg: at most 1 GiB of pinned host memory per direction
+
+# --workload: c2 (default) is the driver's bench line; c4 and c5 are SURVEY §8d's
+# multi-GPU rows, runnable at any N (block-range shards of a fixed total).
+WORKLOADS = {
+    "c2": {"per_gpu": BLOCKS_PER_GPU, "total": None, "roundtrip": False, "scaling": "weak",
+           "desc": WORKLOAD},
+    "c4": {"per_gpu": None, "total": 1 << 30, "roundtrip": False, "scaling": "strong",
+           "desc": "3DES-EDE ECB encrypt, 8 GiB (2^30 blocks) in total, block-range shards over the GPUs, "
+                   "3-key (SP 800-67 sample keys), synthetic splitmix64 plaintext (BASELINE.json configs[3])"},
+    "c5": {"per_gpu": None, "total": 1 << 33, "roundtrip": True, "scaling": "strong",
+           "desc": "3DES-EDE ECB encrypt-then-decrypt round trip, 64 GiB (2^33 blocks) in total, block-range "
+                   "shards over the GPUs, 3-key, synthetic splitmix64 plaintext (BASELINE.json configs[4]); "
+                   "value = plaintext bytes round-tripped per second"},
+}
 
 
 def env_int(name, default):
@@ -240,9 +255,15 @@ def run_ours(args, rank, world, local_rank):
             dist.barrier()
 
     from paper_2007_10752_b200 import shard
-    total_blocks = BLOCKS_PER_GPU * world
+    wl = WORKLOADS[args.workload]
+    total_blocks = wl["total"] if wl["total"] is not None else wl["per_gpu"] * world
     lo, hi = shard.shard_range(total_blocks, world, rank)
     n = hi - lo
+    free_b, _ = torch.cuda.mem_get_info(dev)
+    if 16 * n + (1 << 30) > free_b:
+        raise SystemExit(f"workload {args.workload}: {16 * n / 2**30:.0f} GiB of buffers per GPU "
+                         f"do not fit in {free_b / 2**30:.0f} GiB free; use more GPUs")
+    launches_per_step = 2 if wl["roundtrip"] else 1
     sched = tdes.key_schedule(*synthetic.KEYS_3KEY)
     x = torch.empty(8 * n, dtype=torch.uint8, device=dev)
     y = torch.empty_like(x)
@@ -262,14 +283,22 @@ def run_ours(args, rank, world, local_rank):
     ev1.synchronize()
     lop3_peak_meas = ops / (ev0.elapsed_time(ev1) * 1e-3) / 1e12   # Tops/s
 
+    def step_launches():
+        """One step: one fused launch (c2, c4) or encrypt + in-place decrypt (c5)."""
+        yield lambda: tdes.ecb_encrypt_ptr(sched, x.data_ptr(), y.data_ptr(), n, handle)
+        if wl["roundtrip"]:
+            yield lambda: tdes.ecb_decrypt_ptr(sched, y.data_ptr(), y.data_ptr(), n, handle)
+
     # ---- warmup ----
     for _ in range(args.warmup):
-        tdes.ecb_encrypt_ptr(sched, x.data_ptr(), y.data_ptr(), n, handle)
+        for launch in step_launches():
+            launch()
     torch.cuda.synchronize()
 
-    # ---- timed region: K steps, one fused launch each ----
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    # ---- timed region: K steps ----
+    nl = args.steps * launches_per_step
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(nl)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(nl)]
     t_begin, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     props = torch.cuda.get_device_properties(dev)
     bus = None
@@ -280,10 +309,13 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
     with sampler:
         t_begin.record(stream)
-        for k in range(args.steps):
-            starts[k].record(stream)
-            tdes.ecb_encrypt_ptr(sched, x.data_ptr(), y.data_ptr(), n, handle)
-            ends[k].record(stream)
+        k = 0
+        for _ in range(args.steps):
+            for launch in step_launches():
+                starts[k].record(stream)
+                launch()
+                ends[k].record(stream)
+                k += 1
         t_end.record(stream)
         torch.cuda.synchronize()
     barrier()
@@ -293,19 +325,24 @@ def run_ours(args, rank, world, local_rank):
     clocks = sampler.summary()
 
     # ---- device-side sanity: decrypt restores the plaintext; digest ----
-    z = torch.empty_like(x)
-    tdes.ecb_decrypt_ptr(sched, y.data_ptr(), z.data_ptr(), n, handle)
-    mismatch = tdes.count_mismatch(z, x)
-    digest = tdes.sum64(y)
-    del z
+    if wl["roundtrip"]:
+        mismatch = tdes.count_mismatch(y, x)       # y = dec(enc(x)) after the last step
+        tdes.ecb_encrypt_ptr(sched, x.data_ptr(), y.data_ptr(), n, handle)
+        digest = tdes.sum64(y)
+    else:
+        digest = tdes.sum64(y)
+        tdes.ecb_decrypt_ptr(sched, y.data_ptr(), y.data_ptr(), n, handle)
+        mismatch = tdes.count_mismatch(y, x)
     mismatch = shard.sum_over_ranks(mismatch)
     digest = shard.sum_u64_over_ranks(digest)
 
     # ---- e2e: same metric through the host-buffer C-ABI call ----
+    # (a bounded prefix of the shard for c4/c5: at most 1 GiB of pinned host memory per direction)
+    ne = min(n, E2E_MAX_BLOCKS)
     del y
     torch.cuda.empty_cache()
-    hin = torch.empty(8 * n, dtype=torch.uint8).pin_memory()
-    hin.copy_(x.cpu())
+    hin = torch.empty(8 * ne, dtype=torch.uint8).pin_memory()
+    hin.copy_(x[:8 * ne].cpu())
     del x
     torch.cuda.empty_cache()
     hout = torch.empty_like(hin).pin_memory()
@@ -318,13 +355,15 @@ def run_ours(args, rank, world, local_rank):
     e0.record(stream)
     for _ in range(e2e_steps):
         pipe.run(sched, hin, hout)
+        if wl["roundtrip"]:
+            pipe.run(sched, hout, hout, decrypt=True)
         for s in pipe.streams:
             stream.wait_stream(s)
     e1.record(stream)
     e1.synchronize()
     e2e_ms = e0.elapsed_time(e1)
     e2e_ms = shard.max_over_ranks(e2e_ms)
-    e2e_value = e2e_steps * total_blocks * 8 / (e2e_ms * 1e-3) / 1e9
+    e2e_value = e2e_steps * ne * world * 8 / (e2e_ms * 1e-3) / 1e9
 
     if rank == 0:
         peaks, peaks_src = read_peaks()
@@ -345,11 +384,12 @@ def run_ours(args, rank, world, local_rank):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "blocks_per_gpu": BLOCKS_PER_GPU,
-                       "bytes_per_gpu": BLOCKS_PER_GPU * 8, "total_blocks": total_blocks,
-                       "op": "encrypt", "keys": "3-key", "parallelism": f"dp{world} (block-range shards)",
-                       "l2": "inputs and outputs 1 GiB per GPU > 126 MB L2; no flush needed",
+            "scaling": wl["scaling"], "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": {"workload": wl["desc"], "name": args.workload, "blocks_per_gpu": n,
+                       "bytes_per_gpu": n * 8, "total_blocks": total_blocks,
+                       "op": "encrypt+decrypt" if wl["roundtrip"] else "encrypt", "keys": "3-key",
+                       "parallelism": f"dp{world} (block-range shards)",
+                       "l2": f"inputs and outputs {n * 8 / 2**30:.2f} GiB per GPU > 126 MB L2; no flush needed",
                        "Gblocks_per_s": value / 8},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tops/s",
                          "frac": achieved / peak,
@@ -366,14 +406,17 @@ def run_ours(args, rank, world, local_rank):
                                  "bytes_per_block": 16, "peak_source": peaks_src},
                          "traffic_source": tsrc},
             "clocks": clocks,
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 8 * n,
-                    "d2h_bytes_per_step": 8 * n,
-                    "how": "tdes_ecb_crypt_host: pinned host in/out, 32 MiB chunks on 3 streams (H2D, kernel, D2H overlapped)",
+            "e2e": {"value": e2e_value, "unit": UNIT,
+                    "h2d_bytes_per_step": 8 * ne * launches_per_step,
+                    "d2h_bytes_per_step": 8 * ne * launches_per_step,
+                    "how": "tdes_ecb_crypt_host: pinned host in/out, 32 MiB chunks on 3 streams (H2D, kernel, D2H overlapped)"
+                           + ("" if ne == n else f"; first {ne} blocks of each shard")
+                           + ("; encrypt then decrypt in place" if wl["roundtrip"] else ""),
                     "steps": e2e_steps},
-            "gpu_launches": args.steps,
+            "gpu_launches": nl,
             "check": {"device_roundtrip_mismatch_blocks": mismatch, "ciphertext_sum64": f"{digest:016x}"},
         }
-        if world == 1 and not args.no_cpu_baseline:
+        if world == 1 and not args.no_cpu_baseline and args.workload == "c2":
             v, used, sample, secs = oracle_rate(args.cpu_seconds, BLOCKS_PER_GPU)
             line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": used, "kind": "oracle",
                                     "sample": sample, "seconds": secs, "host_cores": host_cores()}
@@ -410,6 +453,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS),
+                    help="c2: 1 GiB encrypt per GPU (default, weak scaling); c4: 8 GiB total encrypt; "
+                         "c5: 64 GiB total encrypt+decrypt round trip (strong scaling)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

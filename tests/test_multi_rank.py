@@ -79,3 +79,22 @@ def test_single_process_helpers_are_identity():
     assert shard.shard_range(10, 3, 2) == (6, 10)
     with pytest.raises(ValueError):
         shard.shard_range(10, 3, 3)
+
+
+@pytest.mark.parametrize("workload", ["c2", "c4", "c5"])
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_bench_workloads_shard_the_configured_totals(workload, world):
+    """bench.py --workload: c2 is 1 GiB per GPU (weak); c4/c5 split a fixed total (strong)."""
+    import bench
+    wl = bench.WORKLOADS[workload]
+    total = wl["total"] if wl["total"] is not None else wl["per_gpu"] * world
+    ranges = [synthetic.shard_range(total, world, r) for r in range(world)]
+    assert ranges[0][0] == 0 and ranges[-1][1] == total
+    assert all(a[1] == b[0] for a, b in zip(ranges, ranges[1:]))
+    per = {hi - lo for lo, hi in ranges}
+    if workload == "c2":
+        assert per == {1 << 27}
+    elif workload == "c4":
+        assert total == 1 << 30 and per == {(1 << 30) // world}
+    else:
+        assert total == 1 << 33 and wl["roundtrip"] and per == {(1 << 33) // world}
