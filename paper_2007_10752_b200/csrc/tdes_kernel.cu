@@ -6,10 +6,12 @@
 // one-thread-per-bit design, every thread owns 32 blocks and holds
 // them as 64 bit-planes (plane j = FIPS-renamed bit j of all 32 blocks):
 //
-//   S1 load      32 blocks per thread, coalesced (a warp reads 8 KiB contiguous)
+//   S1 load      a warp's 8 KiB tile (32 blocks per lane): one TMA bulk copy into
+//                shared memory, prefetched during the previous tile, then LDS.128
 //   S2 transpose two 32x32 bit transposes (PRMT for the 16/8 stages)
 //   S3 IP        register renaming (free)
-//   S4 48 rounds key XOR (one IMAD each, FMA pipe), 8 LOP3 S-box circuits, XOR into the
+//   S4 48 rounds key XOR (one IMAD each, FMA pipe; operands from LDCU + a shared-
+//                memory key table), 8 LOP3 S-box circuits, XOR into the
 //                other half; E and P are operand/destination renaming (free);
 //                the three DES stages are fused, IP/FP between them cancel
 //   S6 FP        register renaming (free)
@@ -29,9 +31,10 @@
 
 namespace {
 
-// 12 warps per CTA, one CTA per SM: ptxas then keeps the round in 150 registers
+// 12 warps per CTA, one CTA per SM: ptxas then keeps the round in ~156 registers
 // without spills (A/B on B200, 1 GiB: 384 threads 42.4, 512 threads 42.1,
-// 448 41.6, 256 37.6 Gblk/s).
+// 448 41.6, 256 37.6 Gblk/s; with the shared-memory key table 384 threads 46.3,
+// 448/512 threads 44.8-45.2).
 #ifndef TDES_THREADS
 #define TDES_THREADS 384
 #endif
@@ -49,7 +52,7 @@ constexpr int kTileBlocks = kGroupBlocks * kWords;  // per warp
 #ifndef TDES_ROUND_UNROLL
 #define TDES_ROUND_UNROLL 1
 #endif
-constexpr int kRoundUnroll = TDES_ROUND_UNROLL;
+constexpr int kRoundUnroll = TDES_ROUND_UNROLL;  // two-round bodies per loop iteration (2 measured 2-3% slower)
 // Where the per-thread key operand k of the IMAD key XOR is read from (3DES):
 // 0 = the launch parameters (ptxas emits LDC.64 plus an IMAD.U32 address copy
 //     per load), 1 = a shared-memory copy made at CTA start (one broadcast
@@ -70,27 +73,30 @@ constexpr int kKeySmem = TDES_KSMEM;
 #endif
 constexpr bool kTma = TDES_TMA && kWords == 1;
 constexpr int kWarps = kThreads / 32;
-constexpr unsigned kTileBytes = kTileBlocks * 8u;  // two-round bodies per loop iteration (2 measured 3% slower)
+constexpr unsigned kTileBytes = kTileBlocks * 8u;
 
 thread_local int g_last_cuda_error = 0;
 
-// mulhi.s32(0x7FFFFFFF, s) = (s - 1) / 2 for s = +-1 (tdes_gen::kxor).  Passed
-// as a kernel argument so it lives in a register instead of being folded into
-// an immediate (which would force s out of the uniform datapath).
+// mulhi.s32(0x7FFFFFFF, s) = (s - 1) / 2 for s = +-1 (tdes_gen::kxor with
+// MULHI, and the split kernel's k).  Passed as a kernel argument so it lives in a
+// register instead of being folded into an immediate (which would force s out of
+// the uniform datapath).
 constexpr uint32_t kMulhiC = 0x7FFFFFFFu;
 
 // Launch-parameter key material, consumption order (round, E-bit):
 // s = k | 1 (+1 or -1) where k is the subkey bit's all-ones / all-zeros lane
-// mask; the key XOR is rebuilt from s on the FMA pipe (tdes_gen::kxor).
+// mask; x ^ k = x * s + k is one IMAD (tdes_gen::kxor).  s is read as a uniform
+// operand; k is copied to shared memory at CTA start (kKeySmem).
 template <int NROUNDS>
 struct alignas(16) RoundMasks {
   uint32_t s[NROUNDS][48];
-  uint32_t k[NROUNDS][48];  // read only by the MULHI = false key XOR
+  uint32_t k[NROUNDS][48];  // not read by the MULHI key XOR
 };
 
 // The split (latency) kernel takes the subkeys bit-packed (one 48-bit word per
-// round, 384 B for 3DES) and derives s per key bit itself: it is latency bound,
-// and launch cost grows with the parameter size (tools/exp/param_lat.cu).
+// round, 384 B for 3DES) and expands its own s table in shared memory: it is
+// latency bound, and launch cost grows with the parameter size
+// (tools/exp/param_lat.cu).
 template <int NROUNDS>
 struct RoundKeys {
   uint64_t k[NROUNDS];  // bit 47 - b = subkey bit b (E position b), consumption order

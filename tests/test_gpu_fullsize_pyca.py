@@ -96,6 +96,22 @@ def test_config3_256mib_every_block_vs_openssl(tdes, keying, decrypt):
     _full_check(tdes, KEYINGS[keying], synthetic.C3_BLOCKS, decrypt)
 
 
+@pytest.mark.parametrize("decrypt", [False, True])
+def test_single_des_256mib_every_block_vs_openssl(tdes, decrypt):
+    """Single DES (NEXT-1) through des_ecb_*, against OpenSSL TripleDES with K1 = K2 = K3."""
+    k = synthetic.KEYS_1KEY[0]
+    s = tdes.des_key_schedule(k)
+    n = synthetic.C3_BLOCKS
+    x = torch.empty(8 * n, dtype=torch.uint8, device="cuda")
+    tdes.fill_splitmix64(x)
+    y = (tdes.des_ecb_decrypt if decrypt else tdes.des_ecb_encrypt)(x, s)
+    exp = torch.from_numpy(pyca_ecb((k, k, k), n, decrypt)).cuda()  # EDE with K1=K2=K3 = DES
+    bad = tdes.count_mismatch(y, exp)
+    del x, y, exp
+    torch.cuda.empty_cache()
+    assert bad == 0
+
+
 def test_ragged_every_block_vs_openssl(tdes):
     """A size that is neither a multiple of the warp tile nor of the CTA range."""
     _full_check(tdes, synthetic.KEYS_3KEY, (1 << 22) + 12345, False)

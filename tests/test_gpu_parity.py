@@ -129,6 +129,22 @@ def test_single_des_entry_points(tdes, kat_rows):
             assert tdes.des_ecb_encrypt(x, s).cpu().numpy().tobytes() == bytes.fromhex(f[2]), cite
 
 
+@pytest.mark.parametrize("n", [(1 << 20) + 333, 1 << 22])
+def test_single_des_throughput_kernel_vs_oracle(tdes, n):
+    """Single DES above the split-kernel threshold: the throughput kernel (TMA-staged
+    full tiles, ragged last tile) against the oracle on sampled blocks + round trip."""
+    k = "133457799BBCDFF1"
+    s = tdes.des_key_schedule(k)
+    x = torch.empty(8 * n, dtype=torch.uint8, device="cuda")
+    tdes.fill_splitmix64(x)
+    y = tdes.des_ecb_encrypt(x, s)
+    rng = np.random.default_rng(n)
+    idx = np.unique(np.concatenate([rng.integers(0, n, 4096), np.arange(1024), np.arange(n - 1024, n)]))
+    got = y.view(-1, 8)[torch.from_numpy(idx).cuda()].cpu().numpy().reshape(-1)
+    assert np.array_equal(got, oracle.tdes_ecb(k, k, k, synthetic.gather_blocks(idx)))
+    assert tdes.count_mismatch(tdes.des_ecb_decrypt(y, s), x) == 0
+
+
 def test_streams_and_concurrent_keys(tdes):
     n = 20000
     p = synthetic.plaintext_bytes(0, n)
