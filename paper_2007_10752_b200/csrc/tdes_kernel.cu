@@ -31,12 +31,14 @@
 
 namespace {
 
-// 12 warps per CTA, one CTA per SM: ptxas then keeps the round in ~156 registers
-// without spills (A/B on B200, 1 GiB: 384 threads 42.4, 512 threads 42.1,
-// 448 41.6, 256 37.6 Gblk/s; with the shared-memory key table 384 threads 46.3,
-// 448/512 threads 44.8-45.2).
+// 16 warps per CTA, one CTA per SM; ptxas keeps the round in 125 registers
+// without spills (<= 128 for 512 threads).  Warps per CTA measured on B200 with
+// the current kernel (tools/exp/ab_warps.py, us per launch, 12 -> 16 warps):
+// 2^21 blocks 69 -> 61, 2^22 121 -> 111, 2^24 373 -> 370, 2^27 2873 -> 2849;
+// 8-11 warps slower everywhere above 2^21.  (Before the TMA staging cut the
+// register count from 156, 12 warps were best.)
 #ifndef TDES_THREADS
-#define TDES_THREADS 384
+#define TDES_THREADS 512
 #endif
 #ifndef TDES_WORDS
 #define TDES_WORDS 1
