@@ -51,10 +51,15 @@ constexpr int kWords = TDES_WORDS;
 constexpr int kGroupBlocks = 32 * 32;  // one 32-block group per lane: 1024 blocks = 8 KiB per warp
 constexpr int kBlocksPerThread = 32 * kWords;
 constexpr int kTileBlocks = kGroupBlocks * kWords;  // per warp
+// Two-round bodies per loop iteration of the 3DES round loop (single DES: 1).
+// Measured on B200, 1 GiB, current kernel: 1 -> 2 (a 21 KB body) 374 -> 377 GB/s;
+// 3 (33 KB) 363, 4 (40 KB) 352: beyond the 32 KB L1.5 instruction cache.  (Before the TMA staging / 16-warp CTA, 2 was 2-3%
+// slower: the body then had to share the instruction cache with more warps'
+// divergent positions.)
 #ifndef TDES_ROUND_UNROLL
-#define TDES_ROUND_UNROLL 1
+#define TDES_ROUND_UNROLL 2
 #endif
-constexpr int kRoundUnroll = TDES_ROUND_UNROLL;  // two-round bodies per loop iteration (2 measured 2-3% slower)
+constexpr int kRoundUnroll3 = TDES_ROUND_UNROLL;
 // Where the per-thread key operand k of the IMAD key XOR is read from (3DES):
 // 0 = the launch parameters (ptxas emits LDC.64 plus an IMAD.U32 address copy
 //     per load), 1 = a shared-memory copy made at CTA start (one broadcast
@@ -339,7 +344,8 @@ __device__ __forceinline__ void crypt_tile(const uint2* in, uint2* out, size_t b
   // the instruction cache.  The middle stage starts on the half the first one
   // updated last, so at each stage boundary the halves swap
   // register roles and the same A-then-B body continues.
-#pragma unroll kRoundUnroll
+  constexpr int kUnroll = NSTAGES == 3 ? kRoundUnroll3 : 1;
+#pragma unroll kUnroll
   for (int r = 0; r < 16 * NSTAGES; r += 2) {
     if (NSTAGES == 3 && (r == 16 || r == 32)) tdes_gen::swap_halves(P);
     if (kKeySmem == 0 || kUseMulhi<NSTAGES>) {
