@@ -46,11 +46,11 @@ __device__ __forceinline__ void stage(uint32_t (&P)[64], const RM& mk, int r0) {
 #pragma unroll 1
   for (int r = r0; r < r0 + 16; r += 2) {
     if (START_A) {
-      tdes_gen::round_A(P, mk.s[r], mk.k[r]);
-      tdes_gen::round_B(P, mk.s[r + 1], mk.k[r + 1]);
+      tdes_gen::round_A<false>(P, mk.s[r], mk.k[r], 0u);
+      tdes_gen::round_B<false>(P, mk.s[r + 1], mk.k[r + 1], 0u);
     } else {
-      tdes_gen::round_B(P, mk.s[r], mk.k[r]);
-      tdes_gen::round_A(P, mk.s[r + 1], mk.k[r + 1]);
+      tdes_gen::round_B<false>(P, mk.s[r], mk.k[r], 0u);
+      tdes_gen::round_A<false>(P, mk.s[r + 1], mk.k[r + 1], 0u);
     }
   }
 }
