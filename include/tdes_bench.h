@@ -58,6 +58,23 @@ int tdes_ecb_crypt_mode(const tdes_schedule *s, int decrypt, const void *in, voi
  * kernel (its occupancy), for grid accounting. */
 int tdes_device_geometry(int *num_sms, int *ctas_per_sm);
 
+/* Host only (no GPU needed; for the CPU emulator test): the key operands the 3DES
+ * throughput kernel receives for schedule s and direction decrypt (0/1), with the
+ * planes' pending masks folded in (DESIGN.md §6 "mask folding").  Writes up to
+ * out_words uint32 words to out, in this order:
+ *   s[48][stride], k[48][stride]   combined operands of the E-positions that need
+ *                                  a key IMAD (slots 0..slots-1 per round; the
+ *                                  slot -> E-position map is the generator's plan)
+ *   d[48][dstride]                 masks folded by the unfused outputs
+ *   fix_s[3][nfree], fix_k[3][nfree]  priming of round A's free positions before
+ *                                  round 0 and after the swaps at rounds 16 and 32
+ *   fin_s[64], fin_k[64]           final unmasking per plane
+ * and stores the total word count in *words (also when out is NULL or too small:
+ * then nothing is written and TDES_ERR_WORKSPACE is returned).  *geom (if not NULL)
+ * receives {slots, stride, nfree, dstride}. */
+int tdes_fold_operands(const tdes_schedule *s, int decrypt, uint32_t *out, size_t out_words,
+                       size_t *words, int *geom);
+
 #ifdef __cplusplus
 }
 #endif

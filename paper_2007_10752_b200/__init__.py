@@ -79,6 +79,8 @@ def _load():
         "tdes_paper_ecb": ([vp, vp, vp, sz, ctypes.c_int, vp, sz, vp], ctypes.c_int),
         "tdes_ecb_crypt_mode": ([ctypes.POINTER(TdesSchedule), ctypes.c_int, vp, vp, sz, ctypes.c_int, vp],
                                 ctypes.c_int),
+        "tdes_fold_operands": ([ctypes.POINTER(TdesSchedule), ctypes.c_int, vp, sz, ctypes.POINTER(sz),
+                                ctypes.POINTER(ctypes.c_int)], ctypes.c_int),
     }
     for name, (argtypes, restype) in sig.items():
         fn = getattr(lib, name)
@@ -94,7 +96,7 @@ EXPORTS = ("tdes_key_schedule", "tdes_ecb_encrypt", "tdes_ecb_decrypt", "des_key
            "des_ecb_encrypt", "des_ecb_decrypt", "tdes_ecb_crypt_host", "tdes_get_kernel_info",
            "tdes_strerror", "tdes_last_cuda_error", "tdes_fill_splitmix64", "tdes_sum64",
            "tdes_count_mismatch", "tdes_lop3_peak", "tdes_device_geometry", "tdes_paper_ecb",
-           "tdes_ecb_crypt_mode")
+           "tdes_ecb_crypt_mode", "tdes_fold_operands")
 
 MODE_AUTO, MODE_THROUGHPUT, MODE_SPLIT = 0, 1, 2
 
@@ -234,6 +236,28 @@ def kernel_info() -> KernelInfo:
     k = KernelInfo()
     _check(_lib.tdes_get_kernel_info(ctypes.byref(k)), "tdes_get_kernel_info")
     return k
+
+
+def fold_operands(sched: TdesSchedule, decrypt=False) -> dict:
+    """Host-side key operands of the 3DES throughput kernel (mask folding; no GPU needed).
+
+    Returns numpy uint32 arrays s, k [48, stride], d [48, dstride], fix_s, fix_k
+    [3, nfree], fin_s, fin_k [64] and the geometry (include/tdes_bench.h)."""
+    import numpy as np
+    words = ctypes.c_size_t()
+    geom = (ctypes.c_int * 4)()
+    _lib.tdes_fold_operands(ctypes.byref(sched), int(bool(decrypt)), None, 0, ctypes.byref(words), geom)
+    buf = np.zeros(words.value, dtype=np.uint32)
+    _check(_lib.tdes_fold_operands(ctypes.byref(sched), int(bool(decrypt)), buf.ctypes.data, buf.size,
+                                   ctypes.byref(words), geom), "tdes_fold_operands")
+    slots, stride, nfree, dstride = list(geom)
+    out, o = {"slots": slots, "stride": stride, "nfree": nfree, "dstride": dstride}, 0
+    for name, shape in (("s", (48, stride)), ("k", (48, stride)), ("d", (48, dstride)), ("fix_s", (3, nfree)),
+                        ("fix_k", (3, nfree)), ("fin_s", (64,)), ("fin_k", (64,))):
+        n = int(np.prod(shape))
+        out[name] = buf[o:o + n].reshape(shape)
+        o += n
+    return out
 
 
 def device_geometry() -> tuple[int, int]:

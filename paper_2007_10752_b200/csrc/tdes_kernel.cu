@@ -94,10 +94,20 @@ constexpr uint32_t kMulhiC = 0x7FFFFFFFu;
 // s = k | 1 (+1 or -1) where k is the subkey bit's all-ones / all-zeros lane
 // mask; x ^ k = x * s + k is one IMAD (tdes_gen::kxor).  s is read as a uniform
 // operand; k is copied to shared memory at CTA start (kKeySmem).
+//
+// Mask folding: the planes carry pending uniform masks that the
+// host tracks (build_masks), so s/k are the combined "pending mask ^ key bit"
+// operands of the E-positions that still need a key IMAD (tdes_gen::kKeySlots of
+// 48), d are the masks the unfused outputs fold into their planes, fix the
+// operands that prime round A's free positions before round 0 and after each
+// stage-boundary swap, fin the final unmasking of all 64 planes.
 template <int NROUNDS>
 struct alignas(16) RoundMasks {
-  uint32_t s[NROUNDS][48];
-  uint32_t k[NROUNDS][48];  // not read by the MULHI key XOR
+  uint32_t s[NROUNDS][tdes_gen::kKeyStride];
+  uint32_t k[NROUNDS][tdes_gen::kKeyStride];  // not read by the MULHI key XOR
+  uint32_t d[NROUNDS][tdes_gen::kDeltaStride];
+  uint32_t fix_s[3][tdes_gen::kFoldFree], fix_k[3][tdes_gen::kFoldFree];
+  uint32_t fin_s[64], fin_k[64];
 };
 
 // The split (latency) kernel takes the subkeys bit-packed (one 48-bit word per
@@ -152,12 +162,26 @@ __device__ __forceinline__ void bitstage(uint32_t (&a)[32], uint32_t m) {
 // In-register 32x32 bit-matrix transpose: a[i] bit j <-> a[j] bit i.
 // Stage s swaps bit s of the row and column index; s = 16 and 8 are whole
 // half-words / bytes and run as one PRMT per output word.
+#ifndef TDES_T16_FMA
+#define TDES_T16_FMA 0
+#endif
+__device__ __forceinline__ uint32_t imad(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
 __device__ __forceinline__ void transpose32(uint32_t (&a)[32]) {
 #pragma unroll
   for (int k = 0; k < 16; ++k) {
     const uint32_t lo = a[k], hi = a[k + 16];
-    a[k] = __byte_perm(lo, hi, 0x5410);
-    a[k + 16] = __byte_perm(lo, hi, 0x7632);
+    if (TDES_T16_FMA) {  // half-word swap on the FMA pipe: 5 IMADs instead of 2 PRMTs
+      const uint32_t lh = shr_fma<16>(lo), hh = shr_fma<16>(hi);
+      a[k] = imad(hi, 0x10000u, imad(lh, 0xFFFF0000u, lo));  // (lo & 0xFFFF) | hi << 16
+      a[k + 16] = imad(hh, 0x10000u, lh);                    // lo >> 16 | (hi & 0xFFFF0000)
+    } else {
+      a[k] = __byte_perm(lo, hi, 0x5410);
+      a[k + 16] = __byte_perm(lo, hi, 0x7632);
+    }
   }
 #pragma unroll
   for (int k = 0; k < 32; ++k) {
@@ -345,17 +369,25 @@ __device__ __forceinline__ void crypt_tile(const uint2* in, uint2* out, size_t b
   // updated last, so at each stage boundary the halves swap
   // register roles and the same A-then-B body continues.
   constexpr int kUnroll = NSTAGES == 3 ? kRoundUnroll3 : 1;
+  constexpr int kKq = tdes_gen::kKeyStride / 4;  // uint4 key vectors per round in shared memory
+  tdes_gen::fold_fixup_A<kUseMulhi<NSTAGES>>(P, mk.fix_s[0], mk.fix_k[0], c);
 #pragma unroll kUnroll
   for (int r = 0; r < 16 * NSTAGES; r += 2) {
-    if (NSTAGES == 3 && (r == 16 || r == 32)) tdes_gen::swap_halves(P);
+    if (NSTAGES == 3 && (r == 16 || r == 32)) {
+      tdes_gen::swap_halves(P);
+      tdes_gen::fold_fixup_A<kUseMulhi<NSTAGES>>(P, mk.fix_s[r >> 4], mk.fix_k[r >> 4], c);
+    }
+    const uint2* d0 = reinterpret_cast<const uint2*>(mk.d[r]);  // two masks per uniform load
+    const uint2* d1 = reinterpret_cast<const uint2*>(mk.d[r + 1]);
     if (kKeySmem == 0 || kUseMulhi<NSTAGES>) {
-      tdes_gen::round_A<kUseMulhi<NSTAGES>>(P, mk.s[r], mk.k[r], c);
-      tdes_gen::round_B<kUseMulhi<NSTAGES>>(P, mk.s[r + 1], mk.k[r + 1], c);
+      tdes_gen::round_A<kUseMulhi<NSTAGES>>(P, mk.s[r], mk.k[r], d0, c);
+      tdes_gen::round_B<kUseMulhi<NSTAGES>>(P, mk.s[r + 1], mk.k[r + 1], d1, c);
     } else {
-      tdes_gen::round_A<false>(P, mk.s[r], ksm + 12 * r, c);
-      tdes_gen::round_B<false>(P, mk.s[r + 1], ksm + 12 * (r + 1), c);
+      tdes_gen::round_A<false>(P, mk.s[r], ksm + kKq * r, d0, c);
+      tdes_gen::round_B<false>(P, mk.s[r + 1], ksm + kKq * (r + 1), d1, c);
     }
   }
+  tdes_gen::fold_unmask<kUseMulhi<NSTAGES>>(P, mk.fin_s, mk.fin_k, c);
   V Q[64];
   tdes_gen::output_planes(P, Q);
   // ---- S7: back to blocks, store ----
@@ -382,7 +414,7 @@ __global__ void __launch_bounds__(kThreads, kMinCtasPerSm)
 tdes_ecb_kernel(const uint2* in, uint2* out, size_t nblocks,
                 const __grid_constant__ RoundMasks<16 * NSTAGES> mk, uint32_t c) {
   __shared__ unsigned int next_tile;
-  constexpr int kKeyVecs = 12 * 16 * NSTAGES;  // 48 key words per round as uint4
+  constexpr int kKeyVecs = tdes_gen::kKeyStride / 4 * 16 * NSTAGES;  // key words as uint4
   __shared__ uint4 ksm[kKeySmem == 0 || kUseMulhi<NSTAGES> ? 1 : kKeyVecs];  // k, 9 KiB for 3DES
   const unsigned lane = threadIdx.x & 31u;
   const size_t ntiles = (nblocks + kTileBlocks - 1) / kTileBlocks;
@@ -647,6 +679,59 @@ int check_buffers(const void* in, const void* out, size_t nblocks) {
 // 1024-block tiles, the throughput kernel above (measured crossover).
 constexpr size_t kSplitMaxTiles = 296;
 
+// Host side of mask folding: simulate the planes' pending masks M through the
+// fused rounds exactly as the kernel applies them (fix-ups, rounds, swaps) and
+// emit the operands.  Round r is round_A for even r, round_B for odd r; a free
+// E-position of round r reads its plane as is, which is correct because the
+// previous round's unfused output (or a fix-up) set that plane's mask to the key
+// bit of exactly that position.
+template <int NSTAGES>
+void build_masks(const uint32_t (*masks)[48], RoundMasks<16 * NSTAGES>& mk) {
+  using namespace tdes_gen;
+  constexpr int NR = 16 * NSTAGES;
+  memset(&mk, 0, sizeof mk);
+  uint32_t M[64] = {0};
+  auto key = [&](int r, int pos) { return masks[r][pos] ? 0xFFFFFFFFu : 0u; };
+  auto boundary = [&](int r) { return NSTAGES == 3 && (r == 16 || r == 32); };
+  auto fixup = [&](int b, int r) {  // prime round_A's free positions for round r
+    for (int t = 0; t < kFoldFree; ++t) {
+      const int pos = kFoldFreePos[0][t], j = kFoldSrc[0][pos];
+      const uint32_t v = M[j] ^ key(r, pos);
+      mk.fix_s[b][t] = v | 1u;
+      mk.fix_k[b][t] = v;
+      M[j] = key(r, pos);
+    }
+  };
+  fixup(0, 0);
+  for (int r = 0; r < NR; ++r) {
+    const int x = r & 1;
+    if (boundary(r)) {
+      for (int t = 0; t < 32; ++t) {
+        const uint32_t tmp = M[kHalfA[t]];
+        M[kHalfA[t]] = M[kHalfB[t]];
+        M[kHalfB[t]] = tmp;
+      }
+      fixup(r >> 4, r);
+    }
+    for (int q = 0; q < kKeySlots; ++q) {
+      const int pos = kFoldKeyPos[x][q];
+      const uint32_t v = M[kFoldSrc[x][pos]] ^ key(r, pos);
+      mk.s[r][q] = v | 1u;  // s = k | 1
+      mk.k[r][q] = v;
+    }
+    for (int u = 0; u < kFoldFree; ++u) {
+      const int j = kFoldUDst[x][u];
+      const uint32_t want = r + 1 < NR && !boundary(r + 1) ? key(r + 1, kFoldUNext[x][u]) : M[j];
+      mk.d[r][u] = M[j] ^ want;
+      M[j] = want;
+    }
+  }
+  for (int j = 0; j < 64; ++j) {
+    mk.fin_s[j] = M[j] | 1u;
+    mk.fin_k[j] = M[j];
+  }
+}
+
 // mode: 0 auto, 1 throughput kernel, 2 split (latency) kernel.
 template <int NSTAGES>
 int launch(const uint32_t (*masks)[48], const void* in, void* out, size_t nblocks,
@@ -676,11 +761,7 @@ int launch(const uint32_t (*masks)[48], const void* in, void* out, size_t nblock
     return e == cudaSuccess ? TDES_OK : cuda_fail(e);
   }
   RoundMasks<16 * NSTAGES> mk;
-  const uint32_t* m = &masks[0][0];
-  for (int i = 0; i < 16 * NSTAGES * 48; ++i) {  // masks are 0 or ~0 (tdes_key_schedule)
-    (&mk.k[0][0])[i] = m[i] ? 0xFFFFFFFFu : 0u;
-    (&mk.s[0][0])[i] = (&mk.k[0][0])[i] | 1u;  // s = k | 1
-  }
+  build_masks<NSTAGES>(masks, mk);
   // one resident CTA per SM; with fewer tiles than SMs, one tile per CTA
   const size_t ntiles = (nblocks + kTileBlocks - 1) / kTileBlocks;
   const int occ = vec4 ? occupancy<NSTAGES, true>(dev) : occupancy<NSTAGES, false>(dev);
@@ -773,6 +854,24 @@ extern "C" int tdes_get_kernel_info(tdes_kernel_info* out) {
 }
 
 extern "C" int tdes_last_cuda_error(void) { return g_last_cuda_error; }
+
+extern "C" int tdes_fold_operands(const tdes_schedule* s, int decrypt, uint32_t* out, size_t out_words,
+                                  size_t* words, int* geom) {
+  if (!s || !words || (decrypt != 0 && decrypt != 1)) return TDES_ERR_INVALID_ARG;
+  static_assert(sizeof(RoundMasks<48>) % sizeof(uint32_t) == 0, "word-sized layout");
+  *words = sizeof(RoundMasks<48>) / sizeof(uint32_t);
+  if (geom) {
+    geom[0] = tdes_gen::kKeySlots;
+    geom[1] = tdes_gen::kKeyStride;
+    geom[2] = tdes_gen::kFoldFree;
+    geom[3] = tdes_gen::kDeltaStride;
+  }
+  if (!out || out_words < *words) return TDES_ERR_WORKSPACE;
+  RoundMasks<48> mk;
+  build_masks<3>(s->mask[decrypt], mk);
+  memcpy(out, &mk, sizeof mk);
+  return TDES_OK;
+}
 
 extern "C" int tdes_device_geometry(int* sms, int* ctas_per_sm) {
   if (!sms || !ctas_per_sm) return TDES_ERR_INVALID_ARG;

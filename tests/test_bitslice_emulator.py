@@ -151,3 +151,84 @@ def test_emulator_known_answer(gen, kat_rows):
     buf[:24] = np.frombuffer(pts, np.uint8)
     got = emulate(man, circs, buf, key_masks(bytes.fromhex(k1), bytes.fromhex(k2), bytes.fromhex(k3), False))
     assert got[:24].tobytes() == cts
+
+
+def emulate_kernel(circs, blocks_u8, ops):
+    """The throughput kernel's exact structure (tdes_kernel.cu crypt_tile): fold
+    fix-up, 24 x (round_A, round_B) with swap_halves + fix-up at rounds 16 and 32,
+    free E-positions read as is, unfused outputs XOR their uniform mask, final
+    unmask -- with the operands the C++ host code computes (tdes_fold_operands)."""
+    plan = gen_tdes.fold_plan(circs)
+    a_idx, b_idx = gen_tdes.A_IDX, gen_tdes.B_IDX
+    w = blocks_u8.view("<u4").reshape(-1, 32, 2)
+    P = transpose32([w[:, i, 0].copy() for i in range(32)]) + transpose32([w[:, i, 1].copy() for i in range(32)])
+    uidx = {go: u for u, go in enumerate(plan["unf"])}
+
+    def fixup(b):
+        for t, pos in enumerate(plan["A"]["free"]):
+            j = plan["A"]["src"][pos]
+            assert ops["fix_k"][b, t] | 1 == ops["fix_s"][b, t]
+            P[j] = P[j] ^ np.uint32(ops["fix_k"][b, t])
+
+    def rnd(half, r):
+        pl = plan[half]
+        slot = {i: q for q, i in enumerate(pl["keypos"])}
+        for g in range(8):
+            xs = []
+            for i in range(6):
+                pos = 6 * g + i
+                x = P[pl["src"][pos]]
+                if pos in slot:
+                    x = x ^ np.uint32(ops["k"][r, slot[pos]])
+                xs.append(x)
+            sig = list(xs)
+            for lut, a, b, c in circs[g]["gates"]:
+                sig.append(lut_np(lut, sig[a], sig[b], sig[c]))
+            neg = circs[g].get("neg") or [0, 0, 0, 0]
+            fuse = circs[g].get("fuse") or [None] * 4
+            for o in range(4):
+                d = gen_tdes.out_plane(half, g, o)
+                if fuse[o] is not None:
+                    fu, fv, h = fuse[o]
+                    v = np.zeros_like(sig[fu])
+                    for q in range(4):
+                        if (h >> q) & 1:
+                            v |= (sig[fu] if q & 2 else ~sig[fu]) & (sig[fv] if q & 1 else ~sig[fv])
+                else:
+                    v = sig[circs[g]["outputs"][o]]
+                    v = (~v if neg[o] else v) ^ np.uint32(ops["d"][r, uidx[(g, o)]])
+                P[d] = P[d] ^ v
+
+    fixup(0)
+    for r in range(0, 48, 2):
+        if r in (16, 32):
+            for a, b in zip(a_idx, b_idx):
+                P[a], P[b] = P[b], P[a]
+            fixup(r >> 4)
+        rnd("A", r)
+        rnd("B", r + 1)
+    for j in range(64):
+        P[j] = P[j] ^ np.uint32(ops["fin_k"][j])
+    Q = [P[gen_tdes.OUT_SRC[k]] for k in range(64)]
+    ox, oy = transpose32(Q[:32]), transpose32(Q[32:])
+    out = np.empty_like(w)
+    for i in range(32):
+        out[:, i, 0] = ox[i]
+        out[:, i, 1] = oy[i]
+    return out.reshape(-1).view(np.uint8)
+
+
+@pytest.mark.parametrize("keys", [synthetic.KEYS_3KEY, synthetic.KEYS_2KEY, synthetic.KEYS_1KEY,
+                                  ("0101010101010101", "FEFEFEFEFEFEFEFE", "E0E0E0E0F1F1F1F1")])
+@pytest.mark.parametrize("decrypt", [False, True])
+def test_kernel_structure_with_folded_masks_matches_oracle(gen, keys, decrypt):
+    """Mask folding end to end on CPU: the C++ host operands + the generated round
+    structure (free positions, unfused-output masks, boundary fix-ups) == oracle."""
+    import paper_2007_10752_b200 as tdes
+    _, circs = gen
+    ops = tdes.fold_operands(tdes.key_schedule(*keys), decrypt)
+    assert ops["slots"] + ops["nfree"] == 48
+    assert np.array_equal(ops["s"], ops["k"] | np.uint32(1))
+    p = synthetic.plaintext_bytes(0, 32 * 8)
+    got = emulate_kernel(circs, p, ops)
+    assert np.array_equal(got, oracle.tdes_ecb(*keys, p, decrypt=decrypt))

@@ -241,9 +241,11 @@ def emit_sbox(g, circ):
     lines = [f"// S{g + 1}: {len(circ['gates'])} lop3 + 4 Feistel XOR ({nf} of them fused with the output's"
              f" final 2-input join) = {circuit_cost(circ)} ALU ops ({circ['source']})",
              "// Inputs x0..x5 = S-box bits b1..b6; each output is XORed into its destination plane.",
+             "// m0..m3: uniform masks folded into the unfused outputs' XOR (mask folding).",
              "template <class V>",
              f"__device__ __forceinline__ void sbox{g + 1}(V x0, V x1, V x2, V x3, V x4, V x5,",
-             "    V& d0, V& d1, V& d2, V& d3) {"]
+             "    V& d0, V& d1, V& d2, V& d3, uint32_t m0 = 0u, uint32_t m1 = 0u, uint32_t m2 = 0u,",
+             "    uint32_t m3 = 0u) {"]
 
     def name(s):
         return f"x{s}" if s < 6 else f"t{s - 6}"
@@ -256,33 +258,127 @@ def emit_sbox(g, circ):
             lines.append(f"  d{o} = lop3<0x{fused_lut(f[2]):02x}>(d{o}, {name(f[0])}, {name(f[1])});"
                          f"  // d ^= h(u, v), h = 0x{f[2]:x}")
         else:
-            # a complemented output costs nothing: the XOR becomes an XNOR (one LOP3)
-            lines.append(f"  d{o} ^= {'~' if neg[o] else ''}{name(s)};")
+            # a complemented output costs nothing: the XOR becomes an XNOR (one LOP3),
+            # and the free third LOP3 input takes the uniform mask m (mask folding)
+            lines.append(f"  d{o} = xor3<{1 if neg[o] else 0}>(d{o}, {name(s)}, m{o});")
+    unused = [o for o in range(4) if fuse[o] is not None]
+    if unused:
+        lines.append("  (void)" + ", (void)".join(f"m{o}" for o in unused) + ";")
     lines.append("}")
     return "\n".join(lines)
 
 
-def emit_round(half):
-    dst, src = (A_IDX, B_IDX) if half == "A" else (B_IDX, A_IDX)
-    # inverse of P: S-output bit m feeds f position pinv[m]
+def half_maps(half):
+    """(dst planes, src planes) of the round function updating `half`."""
+    return (A_IDX, B_IDX) if half == "A" else (B_IDX, A_IDX)
+
+
+def out_plane(half, g, o):
+    """Plane that output o of S-box g writes in the round updating `half`."""
     pinv = [None] * 32
     for i, m in enumerate(P_SRC):
         pinv[m] = i
+    return half_maps(half)[0][pinv[4 * g + o]]
+
+
+def fold_plan(circs):
+    """Mask folding.  Planes carry a pending uniform mask M (known on
+    the host); an unfused output's XOR has a free third LOP3 input, so while it
+    updates plane j it can also set M[j] to the key bit of one E-position of the
+    next round that reads j -- that position then needs no key IMAD.
+
+    Returns per half (0 = round A, 1 = round B): the unfused outputs [(g, o)], the
+    plane each writes, the next-round E-position each designates, the free
+    (designated) E-positions of the round, and the remaining key positions."""
+    unf = [(g, o) for g in range(8) for o in range(4) if (circs[g].get("fuse") or [None] * 4)[o] is None]
+    plan = {}
+    for x, half in enumerate("AB"):
+        other = "B" if half == "A" else "A"
+        osrc = half_maps(other)[1]
+        udst = [out_plane(half, g, o) for g, o in unf]
+        unext = [min(i for i in range(48) if osrc[T.E[i] - 1] == j) for j in udst]
+        plan[half] = {"udst": udst, "unext": unext}
+    for x, half in enumerate("AB"):
+        other = "B" if half == "A" else "A"
+        free = sorted(plan[other]["unext"])
+        plan[half]["free"] = free
+        plan[half]["keypos"] = [i for i in range(48) if i not in free]
+        plan[half]["src"] = [half_maps(half)[1][T.E[i] - 1] for i in range(48)]
+    plan["unf"] = unf
+    return plan
+
+
+def emit_round(half, plan):
+    dst, src = half_maps(half)
+    pl = plan[half]
+    slot = {i: q for q, i in enumerate(pl["keypos"])}
+    uidx = {go: u for u, go in enumerate(plan["unf"])}
     lines = [f"// One Feistel round updating half {half}: {half} ^= P(S(E(other) ^ K)).",
-             "// Key XOR on the FMA pipe (kxor): S = the round's 48 s = k | 1 values, K = the",
-             "// masks k (read only when MULHI = false), c = 0x7FFFFFFF.",
-             "// S and K point to uint32_t or uint4 arrays (kat reads word i of either).",
-             "template <bool MULHI, class V, class SP, class KP>",
+             "// Key XOR on the FMA pipe (kxor): S = the round's kKeySlots s = k | 1 values, K = the",
+             "// masks k (read only when MULHI = false), c = 0x7FFFFFFF.  E-positions "
+             f"{pl['free']} read their plane",
+             "// as is (mask folding: its pending mask already equals the key bit); D = the masks",
+             "// the unfused outputs fold into their planes.",
+             "// S, K, D point to uint32_t or uint4 arrays (kat reads word i of either).",
+             "template <bool MULHI, class V, class SP, class KP, class DP>",
              f"__device__ __forceinline__ void round_{half}(V (&P)[64], const SP* __restrict__ S,",
-             "                                        const KP* __restrict__ K, uint32_t c) {"]
+             "                                        const KP* __restrict__ K, const DP* __restrict__ D, uint32_t c) {"]
     for g in range(8):
-        xs = [f"kxor<MULHI>(P[{src[T.E[6 * g + i] - 1]}], kat<{6 * g + i}>(S), MULHI ? 0u : kat<{6 * g + i}>(K), c)"
-              for i in range(6)]
-        ds = [f"P[{dst[pinv[4 * g + o]]}]" for o in range(4)]
+        xs = []
+        for i in range(6):
+            pos = 6 * g + i
+            if pos in slot:
+                q = slot[pos]
+                xs.append(f"kxor<MULHI>(P[{src[T.E[pos] - 1]}], kat<{q}>(S), MULHI ? 0u : kat<{q}>(K), c)")
+            else:
+                xs.append(f"P[{src[T.E[pos] - 1]}]")
+        ds = [f"P[{out_plane(half, g, o)}]" for o in range(4)]
+        ms = [f"kat<{uidx[(g, o)]}>(D)" if (g, o) in uidx else "0u" for o in range(4)]
         lines.append(f"  sbox{g + 1}({', '.join(xs)},")
-        lines.append(f"        {', '.join(ds)});")
+        lines.append(f"        {', '.join(ds)}, {', '.join(ms)});")
     lines.append("}")
     return "\n".join(lines)
+
+
+def emit_fold(plan):
+    """Host tables for the mask-folding simulation + the device fix-up/unmask helpers."""
+    nf = len(plan["unf"])
+    nk = 48 - nf
+
+    def arr(name, vals):
+        return f"constexpr uint8_t {name} = {{{', '.join(map(str, vals))}}};"
+    h = ["// ---- mask folding (DESIGN.md §6): tables for the host-side mask simulation ----",
+         f"constexpr int kFoldFree = {nf};          // E-positions per round read without a key IMAD",
+         f"constexpr int kKeySlots = {nk};          // key operands per round",
+         f"constexpr int kKeyStride = {(nk + 3) // 4 * 4};  // per round, padded to uint4",
+         f"constexpr int kDeltaStride = {(nf + 1) // 2 * 2};  // per round, padded to uint2",
+         "// [half][...]: half 0 = round_A (updates A, reads B), 1 = round_B.",
+         arr("kFoldKeyPos[2][kKeySlots]", plan["A"]["keypos"] + plan["B"]["keypos"]),
+         arr("kFoldFreePos[2][kFoldFree]", plan["A"]["free"] + plan["B"]["free"]),
+         arr("kFoldSrc[2][48]", plan["A"]["src"] + plan["B"]["src"]),
+         arr("kFoldUDst[2][kFoldFree]", plan["A"]["udst"] + plan["B"]["udst"]),
+         arr("kFoldUNext[2][kFoldFree]", plan["A"]["unext"] + plan["B"]["unext"]),
+         "// swap_halves exchanges plane kHalfA[t] with kHalfB[t].",
+         arr("kHalfA[32]", A_IDX),
+         arr("kHalfB[32]", B_IDX),
+         "",
+         "// Set the pending masks of round_A's free positions (before round 0 and after",
+         "// the stage-boundary swaps): plane ^= s/k pair t (kxor).",
+         "template <bool MULHI, class V>",
+         "__device__ __forceinline__ void fold_fixup_A(V (&P)[64], const uint32_t* __restrict__ S,",
+         "                                             const uint32_t* __restrict__ K, uint32_t c) {"]
+    for t, i in enumerate(plan["A"]["free"]):
+        j = plan["A"]["src"][i]
+        h.append(f"  P[{j}] = kxor<MULHI>(P[{j}], S[{t}], MULHI ? 0u : K[{t}], c);")
+    h += ["}", "",
+          "// Remove every plane's pending mask (after the last round).",
+          "template <bool MULHI, class V>",
+          "__device__ __forceinline__ void fold_unmask(V (&P)[64], const uint32_t* __restrict__ S,",
+          "                                            const uint32_t* __restrict__ K, uint32_t c) {",
+          "#pragma unroll",
+          "  for (int j = 0; j < 64; ++j) P[j] = kxor<MULHI>(P[j], S[j], MULHI ? 0u : K[j], c);",
+          "}", ""]
+    return h
 
 
 def split_tables():
@@ -375,9 +471,20 @@ def emit_header(circs):
         "  return a[I];",
         "}",
         "template <int I>",
+        "__device__ __forceinline__ uint32_t kat(const uint2* __restrict__ a) {",
+        "  const uint2 v = a[I / 2];",
+        "  return I % 2 == 0 ? v.x : v.y;",
+        "}",
+        "template <int I>",
         "__device__ __forceinline__ uint32_t kat(const uint4* __restrict__ a) {",
         "  const uint4 v = a[I / 4];",
         "  return I % 4 == 0 ? v.x : I % 4 == 1 ? v.y : I % 4 == 2 ? v.z : v.w;",
+        "}",
+        "",
+        "// d ^ t ^ m (NEG: d ^ ~t ^ m) as one LOP3; m is a uniform mask (mask folding).",
+        "template <int NEG>",
+        "__device__ __forceinline__ uint32_t xor3(uint32_t d, uint32_t t, uint32_t m) {",
+        "  return lop3<NEG ? 0x69 : 0x96>(d, t, m);",
         "}",
         "",
         "// W independent 32-block groups per thread: a plane is W words and every op",
@@ -411,6 +518,14 @@ def emit_header(circs):
         "  return d;",
         "}",
         "",
+        "template <int NEG, int W>",
+        "__device__ __forceinline__ Vec<W> xor3(const Vec<W>& d, const Vec<W>& t, uint32_t m) {",
+        "  Vec<W> r;",
+        "#pragma unroll",
+        "  for (int i = 0; i < W; ++i) r.w[i] = xor3<NEG>(d.w[i], t.w[i], m);",
+        "  return r;",
+        "}",
+        "",
         "template <bool MULHI, int W>",
         "__device__ __forceinline__ Vec<W> kxor(const Vec<W>& x, uint32_t s, uint32_t kmem, uint32_t c) {",
         "  uint32_t k = kmem;",
@@ -426,10 +541,12 @@ def emit_header(circs):
     for g, c in enumerate(circs):
         h.append(emit_sbox(g, c))
         h.append("")
-    h.append(emit_round("A"))
+    plan = fold_plan(circs)
+    h.append(emit_round("A", plan))
     h.append("")
-    h.append(emit_round("B"))
+    h.append(emit_round("B", plan))
     h.append("")
+    h += emit_fold(plan)
     h.append("// Exchange the register roles of the halves A (IP left, L0) and B (IP right, R0).")
     h.append("template <class V>")
     h.append("__device__ __forceinline__ void swap_halves(V (&P)[64]) {")
