@@ -66,7 +66,7 @@ int tdes_device_geometry(int *num_sms, int *ctas_per_sm);
  *                                  a key IMAD (slots 0..slots-1 per round; the
  *                                  slot -> E-position map is the generator's plan)
  *   d[48][dstride]                 masks folded by the unfused outputs
- *   fix_s[3][nfree], fix_k[3][nfree]  priming of round A's free positions before
+ *   fix_s[3][dstride], fix_k[3][dstride]  priming of round A's free positions before
  *                                  round 0 and after the swaps at rounds 16 and 32
  *   fin_s[64], fin_k[64]           final unmasking per plane
  * and stores the total word count in *words (also when out is NULL or too small:

@@ -242,7 +242,7 @@ def fold_operands(sched: TdesSchedule, decrypt=False) -> dict:
     """Host-side key operands of the 3DES throughput kernel (mask folding; no GPU needed).
 
     Returns numpy uint32 arrays s, k [48, stride], d [48, dstride], fix_s, fix_k
-    [3, nfree], fin_s, fin_k [64] and the geometry (include/tdes_bench.h)."""
+    [3, dstride], fin_s, fin_k [64] and the geometry (include/tdes_bench.h)."""
     import numpy as np
     words = ctypes.c_size_t()
     geom = (ctypes.c_int * 4)()
@@ -252,8 +252,8 @@ def fold_operands(sched: TdesSchedule, decrypt=False) -> dict:
                                    ctypes.byref(words), geom), "tdes_fold_operands")
     slots, stride, nfree, dstride = list(geom)
     out, o = {"slots": slots, "stride": stride, "nfree": nfree, "dstride": dstride}, 0
-    for name, shape in (("s", (48, stride)), ("k", (48, stride)), ("d", (48, dstride)), ("fix_s", (3, nfree)),
-                        ("fix_k", (3, nfree)), ("fin_s", (64,)), ("fin_k", (64,))):
+    for name, shape in (("s", (48, stride)), ("k", (48, stride)), ("d", (48, dstride)), ("fix_s", (3, dstride)),
+                        ("fix_k", (3, dstride)), ("fin_s", (64,)), ("fin_k", (64,))):
         n = int(np.prod(shape))
         out[name] = buf[o:o + n].reshape(shape)
         o += n

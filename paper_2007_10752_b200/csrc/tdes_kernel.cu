@@ -106,7 +106,7 @@ struct alignas(16) RoundMasks {
   uint32_t s[NROUNDS][tdes_gen::kKeyStride];
   uint32_t k[NROUNDS][tdes_gen::kKeyStride];  // not read by the MULHI key XOR
   uint32_t d[NROUNDS][tdes_gen::kDeltaStride];
-  uint32_t fix_s[3][tdes_gen::kFoldFree], fix_k[3][tdes_gen::kFoldFree];
+  uint32_t fix_s[3][tdes_gen::kDeltaStride], fix_k[3][tdes_gen::kDeltaStride];
   uint32_t fin_s[64], fin_k[64];
 };
 
@@ -369,7 +369,8 @@ __device__ __forceinline__ void crypt_tile(const uint2* in, uint2* out, size_t b
   // updated last, so at each stage boundary the halves swap
   // register roles and the same A-then-B body continues.
   constexpr int kUnroll = NSTAGES == 3 ? kRoundUnroll3 : 1;
-  constexpr int kKq = tdes_gen::kKeyStride / 4;  // uint4 key vectors per round in shared memory
+  constexpr int kKv = tdes_gen::kKeyStride / 4;              // k vectors per round
+  constexpr int kKq = kKv + tdes_gen::kDeltaStride / 4;      // k + d vectors per round in shared memory
   tdes_gen::fold_fixup_A<kUseMulhi<NSTAGES>>(P, mk.fix_s[0], mk.fix_k[0], c);
 #pragma unroll kUnroll
   for (int r = 0; r < 16 * NSTAGES; r += 2) {
@@ -377,14 +378,17 @@ __device__ __forceinline__ void crypt_tile(const uint2* in, uint2* out, size_t b
       tdes_gen::swap_halves(P);
       tdes_gen::fold_fixup_A<kUseMulhi<NSTAGES>>(P, mk.fix_s[r >> 4], mk.fix_k[r >> 4], c);
     }
-    const uint2* d0 = reinterpret_cast<const uint2*>(mk.d[r]);  // two masks per uniform load
-    const uint2* d1 = reinterpret_cast<const uint2*>(mk.d[r + 1]);
     if (kKeySmem == 0 || kUseMulhi<NSTAGES>) {
-      tdes_gen::round_A<kUseMulhi<NSTAGES>>(P, mk.s[r], mk.k[r], d0, c);
-      tdes_gen::round_B<kUseMulhi<NSTAGES>>(P, mk.s[r + 1], mk.k[r + 1], d1, c);
-    } else {
-      tdes_gen::round_A<false>(P, mk.s[r], ksm + kKq * r, d0, c);
-      tdes_gen::round_B<false>(P, mk.s[r + 1], ksm + kKq * (r + 1), d1, c);
+      tdes_gen::round_A<kUseMulhi<NSTAGES>>(P, mk.s[r], mk.k[r], mk.d[r], c);
+      tdes_gen::round_B<kUseMulhi<NSTAGES>>(P, mk.s[r + 1], mk.k[r + 1], mk.d[r + 1], c);
+    } else {  // k and d from the shared-memory table: [round][k | d] as uint4
+      const uint4* t0 = ksm + kKq * r;
+      const uint4* t1 = ksm + kKq * (r + 1);
+      // s as uint2 pairs: every uniform load is 64-bit, also for an odd slot count
+      const uint2* s0 = reinterpret_cast<const uint2*>(mk.s[r]);
+      const uint2* s1 = reinterpret_cast<const uint2*>(mk.s[r + 1]);
+      tdes_gen::round_A<false>(P, s0, t0, t0 + kKv, c);
+      tdes_gen::round_B<false>(P, s1, t1, t1 + kKv, c);
     }
   }
   tdes_gen::fold_unmask<kUseMulhi<NSTAGES>>(P, mk.fin_s, mk.fin_k, c);
@@ -414,7 +418,9 @@ __global__ void __launch_bounds__(kThreads, kMinCtasPerSm)
 tdes_ecb_kernel(const uint2* in, uint2* out, size_t nblocks,
                 const __grid_constant__ RoundMasks<16 * NSTAGES> mk, uint32_t c) {
   __shared__ unsigned int next_tile;
-  constexpr int kKeyVecs = tdes_gen::kKeyStride / 4 * 16 * NSTAGES;  // key words as uint4
+  // shared-memory key table: per round the kKeySlots k operands then the unfused-output masks d
+  constexpr int kKv = tdes_gen::kKeyStride / 4, kDv = tdes_gen::kDeltaStride / 4;
+  constexpr int kKeyVecs = (kKv + kDv) * 16 * NSTAGES;
   __shared__ uint4 ksm[kKeySmem == 0 || kUseMulhi<NSTAGES> ? 1 : kKeyVecs];  // k, 9 KiB for 3DES
   const unsigned lane = threadIdx.x & 31u;
   const size_t ntiles = (nblocks + kTileBlocks - 1) / kTileBlocks;
@@ -423,7 +429,11 @@ tdes_ecb_kernel(const uint2* in, uint2* out, size_t nblocks,
   if (threadIdx.x == 0) next_tile = 0;
   if (kKeySmem != 0 && !kUseMulhi<NSTAGES>) {
     const uint4* k4 = reinterpret_cast<const uint4*>(&mk.k[0][0]);
-    for (int i = threadIdx.x; i < kKeyVecs; i += blockDim.x) ksm[i] = k4[i];
+    const uint4* d4 = reinterpret_cast<const uint4*>(&mk.d[0][0]);
+    for (int i = threadIdx.x; i < kKeyVecs; i += blockDim.x) {
+      const int r = i / (kKv + kDv), q = i % (kKv + kDv);
+      ksm[i] = q < kKv ? k4[r * kKv + q] : d4[r * kDv + q - kKv];
+    }
   }
   extern __shared__ uint4 tma_buf[];  // kTma: [kWarps][kTileBytes / 16], dynamic
   __shared__ uint64_t tma_bar[kWarps];

@@ -172,6 +172,19 @@ def load_searched():
     return best
 
 
+def normalize_outputs(circ):
+    """A fused output h(u, u) is a plain (possibly complemented) signal: write it as an
+    unfused output, which costs the same one LOP3 but leaves that LOP3's third input
+    free for mask folding."""
+    fuse = list(circ.get("fuse") or [None] * 4)
+    outs, neg = list(circ["outputs"]), list(circ.get("neg") or [0, 0, 0, 0])
+    for o in range(4):
+        f = fuse[o]
+        if f is not None and f[0] == f[1] and (f[2] & 9) in (1, 8):
+            outs[o], neg[o], fuse[o] = f[0], 1 if (f[2] & 9) == 1 else 0, None
+    return dict(circ, outputs=outs, neg=neg, fuse=fuse)
+
+
 def choose_circuits(muxtree_only=False):
     searched = {} if muxtree_only else load_searched()
     out = []
@@ -179,7 +192,10 @@ def choose_circuits(muxtree_only=False):
         m = muxtree_circuit(g)
         assert verify_circuit(g, m)
         c = searched.get(g)
-        out.append(c if c is not None and circuit_cost(c) < circuit_cost(m) else m)
+        c = c if c is not None and circuit_cost(c) < circuit_cost(m) else m
+        c = normalize_outputs(c)
+        assert verify_circuit(g, c)
+        out.append(c)
     return out
 
 
@@ -281,6 +297,12 @@ def out_plane(half, g, o):
     return half_maps(half)[0][pinv[4 * g + o]]
 
 
+# At most this many folded positions per round: with 11 (37 key operands per round)
+# ptxas moved the round loop's index and the key loads off the uniform datapath
+# (per-thread LDC instead of LDCU), with 10 or fewer it keeps them uniform.
+FOLD_MAX_FREE = 10
+
+
 def fold_plan(circs):
     """Mask folding.  Planes carry a pending uniform mask M (known on
     the host); an unfused output's XOR has a free third LOP3 input, so while it
@@ -291,6 +313,7 @@ def fold_plan(circs):
     plane each writes, the next-round E-position each designates, the free
     (designated) E-positions of the round, and the remaining key positions."""
     unf = [(g, o) for g in range(8) for o in range(4) if (circs[g].get("fuse") or [None] * 4)[o] is None]
+    unf = unf[:int(os.environ.get("TDES_GEN_MAX_FREE", FOLD_MAX_FREE))]
     plan = {}
     for x, half in enumerate("AB"):
         other = "B" if half == "A" else "A"
@@ -351,7 +374,7 @@ def emit_fold(plan):
          f"constexpr int kFoldFree = {nf};          // E-positions per round read without a key IMAD",
          f"constexpr int kKeySlots = {nk};          // key operands per round",
          f"constexpr int kKeyStride = {(nk + 3) // 4 * 4};  // per round, padded to uint4",
-         f"constexpr int kDeltaStride = {(nf + 1) // 2 * 2};  // per round, padded to uint2",
+         f"constexpr int kDeltaStride = {(nf + 3) // 4 * 4};  // per round, padded to uint4",
          "// [half][...]: half 0 = round_A (updates A, reads B), 1 = round_B.",
          arr("kFoldKeyPos[2][kKeySlots]", plan["A"]["keypos"] + plan["B"]["keypos"]),
          arr("kFoldFreePos[2][kFoldFree]", plan["A"]["free"] + plan["B"]["free"]),
@@ -426,7 +449,8 @@ def emit_header(circs):
         "// Bitsliced DES building blocks for the sm_100a 3DES-ECB kernel.",
         "// Planes: P[32*w + j] holds bit j of little-endian word w of each of the",
         "// thread's 32 blocks (bit i of a plane = block i).",
-        f"// S-box LOP3 total T = {total} per round; per round: 48 key-XOR IMAD (FMA pipe) + T + 32 Feistel-XOR LOP3 (ALU pipe).",
+        f"// S-box LOP3 total T = {total} per round; per round: {48 - len(fold_plan(circs)['unf'])} key-XOR IMAD (FMA pipe; the other"
+        f" {len(fold_plan(circs)['unf'])} E-positions are mask-folded) + T + 32 Feistel-XOR LOP3 (ALU pipe).",
         "#pragma once",
         "#include <stdint.h>",
         "",
