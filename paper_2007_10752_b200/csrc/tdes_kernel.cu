@@ -162,26 +162,12 @@ __device__ __forceinline__ void bitstage(uint32_t (&a)[32], uint32_t m) {
 // In-register 32x32 bit-matrix transpose: a[i] bit j <-> a[j] bit i.
 // Stage s swaps bit s of the row and column index; s = 16 and 8 are whole
 // half-words / bytes and run as one PRMT per output word.
-#ifndef TDES_T16_FMA
-#define TDES_T16_FMA 0
-#endif
-__device__ __forceinline__ uint32_t imad(uint32_t a, uint32_t b, uint32_t c) {
-  uint32_t d;
-  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
-  return d;
-}
 __device__ __forceinline__ void transpose32(uint32_t (&a)[32]) {
 #pragma unroll
   for (int k = 0; k < 16; ++k) {
     const uint32_t lo = a[k], hi = a[k + 16];
-    if (TDES_T16_FMA) {  // half-word swap on the FMA pipe: 5 IMADs instead of 2 PRMTs
-      const uint32_t lh = shr_fma<16>(lo), hh = shr_fma<16>(hi);
-      a[k] = imad(hi, 0x10000u, imad(lh, 0xFFFF0000u, lo));  // (lo & 0xFFFF) | hi << 16
-      a[k + 16] = imad(hh, 0x10000u, lh);                    // lo >> 16 | (hi & 0xFFFF0000)
-    } else {
-      a[k] = __byte_perm(lo, hi, 0x5410);
-      a[k + 16] = __byte_perm(lo, hi, 0x7632);
-    }
+    a[k] = __byte_perm(lo, hi, 0x5410);
+    a[k + 16] = __byte_perm(lo, hi, 0x7632);
   }
 #pragma unroll
   for (int k = 0; k < 32; ++k) {

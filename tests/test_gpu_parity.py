@@ -66,6 +66,34 @@ def test_random_keys_and_data(tdes):
             assert np.array_equal(fn(to_dev(p), s).cpu().numpy(), oracle.tdes_ecb(*ks, p, decrypt=dec))
 
 
+def test_random_keys_throughput_kernel(tdes):
+    """The throughput kernel's key operands depend on the key through mask folding
+    (host-tracked pending plane masks): many random key triples, forced mode 1."""
+    rng = np.random.default_rng(21)
+    for t in range(16):
+        ks = [synthetic.random_key(rng) for _ in range(3)]
+        if t % 4 == 1:
+            ks[2] = ks[0]  # 2-key
+        n = 2048 + int(rng.integers(0, 3000))
+        p = synthetic.random_blocks(rng, n)
+        s = tdes.key_schedule(*ks)
+        for dec in (False, True):
+            got = tdes.ecb_crypt_mode(to_dev(p), s, tdes.MODE_THROUGHPUT, decrypt=dec).cpu().numpy()
+            assert np.array_equal(got, oracle.tdes_ecb(*ks, p, decrypt=dec)), (t, dec)
+
+
+def test_random_keys_single_des_throughput_kernel(tdes):
+    rng = np.random.default_rng(22)
+    n = 310 * 1024 + 17  # above the split-kernel threshold
+    for _ in range(4):
+        k = synthetic.random_key(rng)
+        p = synthetic.random_blocks(rng, n)
+        s = tdes.des_key_schedule(k)
+        c = tdes.des_ecb_encrypt(to_dev(p), s)
+        assert np.array_equal(c.cpu().numpy(), oracle.tdes_ecb(k, k, k, p))
+        assert np.array_equal(tdes.des_ecb_decrypt(c, s).cpu().numpy(), p)
+
+
 def test_known_answers(tdes, kat_rows):
     for kind, f, cite in kat_rows:
         if kind == "TDES":
