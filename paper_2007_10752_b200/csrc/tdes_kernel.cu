@@ -728,6 +728,28 @@ void build_masks(const uint32_t (*masks)[48], RoundMasks<16 * NSTAGES>& mk) {
   }
 }
 
+// build_masks costs ~10 us of host time per call; launches with the same key
+// material (the common case: one key, many launches) reuse the result.  Two
+// entries per thread and variant, so alternating encrypt/decrypt also hits.
+template <int NSTAGES>
+const RoundMasks<16 * NSTAGES>& cached_masks(const uint32_t (*masks)[48]) {
+  struct Entry {
+    uint32_t key[16 * NSTAGES][48];
+    RoundMasks<16 * NSTAGES> mk;
+    bool valid = false;
+  };
+  thread_local Entry cache[2];
+  thread_local int next = 0;
+  for (Entry& e : cache)
+    if (e.valid && memcmp(e.key, masks, sizeof e.key) == 0) return e.mk;
+  Entry& e = cache[next];
+  next ^= 1;
+  memcpy(e.key, masks, sizeof e.key);
+  build_masks<NSTAGES>(masks, e.mk);
+  e.valid = true;
+  return e.mk;
+}
+
 // mode: 0 auto, 1 throughput kernel, 2 split (latency) kernel.
 template <int NSTAGES>
 int launch(const uint32_t (*masks)[48], const void* in, void* out, size_t nblocks,
@@ -756,8 +778,7 @@ int launch(const uint32_t (*masks)[48], const void* in, void* out, size_t nblock
     e = cudaGetLastError();
     return e == cudaSuccess ? TDES_OK : cuda_fail(e);
   }
-  RoundMasks<16 * NSTAGES> mk;
-  build_masks<NSTAGES>(masks, mk);
+  const RoundMasks<16 * NSTAGES>& mk = cached_masks<NSTAGES>(masks);
   // one resident CTA per SM; with fewer tiles than SMs, one tile per CTA
   const size_t ntiles = (nblocks + kTileBlocks - 1) / kTileBlocks;
   const int occ = vec4 ? occupancy<NSTAGES, true>(dev) : occupancy<NSTAGES, false>(dev);
