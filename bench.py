@@ -401,6 +401,7 @@ def run_ours(args, rank, world, local_rank):
                          "peak_microbench": lop3_peak_meas,
                          "frac_of_microbench": achieved / lop3_peak_meas,
                          "kernel_ms_avg": avg_kern_s * 1e3,
+                         "kernel_ms_p10_p50_p90": [round(float(np.percentile(kern_ms, q)), 5) for q in (10, 50, 90)],
                          "hbm": {"achieved_gbs": hbm_gbs, "peak_gbs": float(peaks.get("hbm_gbs", HBM_PEAK_FALLBACK)),
                                  "frac": hbm_gbs / float(peaks.get("hbm_gbs", HBM_PEAK_FALLBACK)),
                                  "bytes_per_block": 16, "peak_source": peaks_src},
