@@ -17,6 +17,10 @@ for mode in (1, 2):                               # throughput and S-box-split k
     tdes.ecb_crypt_mode(x, s, mode, out=y)
     tdes.ecb_crypt_mode(y, s, mode, decrypt=True, out=y)   # in place
 tdes.ecb_encrypt(x[8:8 + 8 * 1000], s, out=y[8:8 + 8 * 1000])   # 8-byte-aligned path
+m = 17 * 1024 + 5                                 # > 16 tiles: the non-specialised split kernel
+xm = torch.empty(8 * m, dtype=torch.uint8, device="cuda")
+tdes.fill_splitmix64(xm)
+tdes.ecb_crypt_mode(xm, s, 2, out=torch.empty_like(xm))
 ds = tdes.des_key_schedule(synthetic.KEYS_1KEY[0])
 tdes.des_ecb_encrypt(x, ds, out=y)
 tdes.PaperBaseline(*synthetic.KEYS_3KEY).run(x[:8 * 64], out=y[:8 * 64])
