@@ -52,13 +52,19 @@ def _pyca_available():
 
 def pyca_ecb(keys, nblocks, decrypt=False) -> np.ndarray:
     """TripleDES-ECB of synthetic blocks [0, nblocks) by OpenSSL, in parallel."""
+    return _pyca_range(keys, 0, nblocks, decrypt)
+
+
+def _pyca_range(keys, first, nblocks, decrypt=False) -> np.ndarray:
+    """TripleDES-ECB of synthetic blocks [first, first + nblocks) by OpenSSL, in parallel."""
     out = np.empty(8 * nblocks, dtype=np.uint8)
-    tasks = [(keys, s, min(CHUNK, nblocks - s), decrypt) for s in range(0, nblocks, CHUNK)]
+    tasks = [(keys, first + s, min(CHUNK, nblocks - s), decrypt) for s in range(0, nblocks, CHUNK)]
     workers = max(1, min(len(tasks), len(os.sched_getaffinity(0))))
     # fork: the workers use only numpy and OpenSSL, never CUDA
     with ProcessPoolExecutor(workers, mp_context=multiprocessing.get_context("fork")) as ex:
         for start, c in ex.map(_pyca_chunk, tasks):
-            out[8 * start:8 * start + len(c)] = np.frombuffer(c, dtype=np.uint8)
+            o = 8 * (start - first)
+            out[o:o + len(c)] = np.frombuffer(c, dtype=np.uint8)
     return out
 
 
@@ -110,6 +116,52 @@ def test_single_des_256mib_every_block_vs_openssl(tdes, decrypt):
     del x, y, exp
     torch.cuda.empty_cache()
     assert bad == 0
+
+
+def test_config4_8gib_every_block_vs_openssl(tdes):
+    """C4's 8 GiB (2^30 blocks) in one launch on one GPU, compared 1 GiB at a time with
+    OpenSSL (the bench's --workload c4 computes the same ciphertext in shards)."""
+    n = synthetic.C4_BLOCKS_TOTAL
+    s = tdes.key_schedule(*synthetic.KEYS_3KEY)
+    x = torch.empty(8 * n, dtype=torch.uint8, device="cuda")
+    tdes.fill_splitmix64(x)
+    y = torch.empty_like(x)
+    tdes.ecb_encrypt(x, s, out=y)
+    del x
+    torch.cuda.empty_cache()
+    step = 1 << 27
+    bad = 0
+    for start in range(0, n, step):
+        exp = torch.from_numpy(_pyca_range(synthetic.KEYS_3KEY, start, step)).cuda()
+        bad += tdes.count_mismatch(y[8 * start:8 * (start + step)], exp)
+        del exp
+    del y
+    torch.cuda.empty_cache()
+    assert bad == 0, f"{bad} of {n} blocks differ from OpenSSL"
+
+
+@pytest.mark.slow
+@pytest.mark.skipif(not os.environ.get("TDES_SLOW_TESTS"), reason="64 GiB x OpenSSL takes ~4 min: set TDES_SLOW_TESTS=1")
+def test_config5_64gib_roundtrip_every_block_vs_openssl(tdes):
+    """C5's 64 GiB (2^33 blocks) on one GPU (128 GiB of HBM): encrypt compared 1 GiB at a
+    time with OpenSSL, then decrypt in place back to the plaintext."""
+    n = synthetic.C5_BLOCKS_TOTAL
+    s = tdes.key_schedule(*synthetic.KEYS_3KEY)
+    x = torch.empty(8 * n, dtype=torch.uint8, device="cuda")
+    tdes.fill_splitmix64(x)
+    y = torch.empty_like(x)
+    tdes.ecb_encrypt(x, s, out=y)
+    step = 1 << 27
+    bad = 0
+    for start in range(0, n, step):
+        exp = torch.from_numpy(_pyca_range(synthetic.KEYS_3KEY, start, step)).cuda()
+        bad += tdes.count_mismatch(y[8 * start:8 * (start + step)], exp)
+        del exp
+    tdes.ecb_decrypt(y, s, out=y)
+    back = tdes.count_mismatch(y, x)
+    del x, y
+    torch.cuda.empty_cache()
+    assert bad == 0 and back == 0, (bad, back)
 
 
 def test_ragged_every_block_vs_openssl(tdes):
