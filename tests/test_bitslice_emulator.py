@@ -197,8 +197,9 @@ def emulate_kernel(circs, blocks_u8, ops):
                 else:
                     v = sig[circs[g]["outputs"][o]]
                     v = ~v if neg[o] else v
-                    if (g, o) in uidx:  # folded: the unfused output's free LOP3 input
-                        v = v ^ np.uint32(ops["d"][r, uidx[(g, o)]])
+                if (g, o) in uidx:  # folded: an unfused output's free LOP3 input, or (for a
+                    # linear fused join) its single-use producer gate's free input
+                    v = v ^ np.uint32(ops["d"][r, uidx[(g, o)]])
                 P[d] = P[d] ^ v
 
     fixup(0)

@@ -251,6 +251,42 @@ def fused_lut(h: int) -> int:
     return sum(1 << k for k in range(8) if ((k >> 2) & 1) ^ ((h >> (k & 3)) & 1))
 
 
+def fold_producers(circ):
+    """Fused outputs d ^= h(u, v) with h linear (XOR/XNOR) whose u or v is a gate with
+    at most two distinct inputs and no other consumer: that gate's free third input can
+    XOR a uniform mask into the output (mask folding).  Returns {o: gate index}."""
+    fuse = circ.get("fuse") or [None] * 4
+    uses = {}
+    for lut, a, b, c in circ["gates"]:
+        for x in {a, b, c}:
+            uses[x] = uses.get(x, 0) + 1
+    for f in fuse:
+        if f is not None:
+            for x in {f[0], f[1]}:
+                uses[x] = uses.get(x, 0) + 1
+    out = {}
+    for o, f in enumerate(fuse):
+        if f is None or f[2] not in (0x6, 0x9):
+            continue
+        for sig in (f[0], f[1]):
+            if sig >= 6 and len({*circ["gates"][sig - 6][1:]}) <= 2 and uses.get(sig, 0) == 1:
+                out[o] = sig - 6
+                break
+    return out
+
+
+def masked_lut(gate):
+    """LOP3 table over (a, b, m) of gate(a, b) ^ m for a gate with two distinct inputs."""
+    lut, *ins = gate
+    dist = sorted(set(ins))
+    a, b = dist[0], dist[-1]
+
+    def f(va, vb):
+        bits = [va if x == a else vb for x in ins]
+        return (lut >> ((bits[0] << 2) | (bits[1] << 1) | bits[2])) & 1
+    return a, b, sum(1 << k for k in range(8) if f((k >> 2) & 1, (k >> 1) & 1) ^ (k & 1))
+
+
 def emit_sbox(g, circ):
     fuse = circ.get("fuse") or [None] * 4
     nf = sum(1 for f in fuse if f is not None)
@@ -265,7 +301,13 @@ def emit_sbox(g, circ):
 
     def name(s):
         return f"x{s}" if s < 6 else f"t{s - 6}"
+    prod = {k: o for o, k in fold_producers(circ).items()}
     for k, (lut, a, b, c) in enumerate(circ["gates"]):
+        if k in prod:  # XOR the output's fold mask into this single-use two-input gate
+            ma, mb, mlut = masked_lut(circ["gates"][k])
+            lines.append(f"  const V t{k} = lop3m<0x{mlut:02x}>({name(ma)}, {name(mb)}, m{prod[k]});"
+                         f"  // 0x{lut:02x}(...) ^ m{prod[k]}")
+            continue
         lines.append(f"  const V t{k} = lop3<0x{lut:02x}>({name(a)}, {name(b)}, {name(c)});")
     neg = circ.get("neg") or [0, 0, 0, 0]
     for o, s in enumerate(circ["outputs"]):
@@ -277,7 +319,7 @@ def emit_sbox(g, circ):
             # a complemented output costs nothing: the XOR becomes an XNOR (one LOP3),
             # and the free third LOP3 input takes the uniform mask m (mask folding)
             lines.append(f"  d{o} = xor3<{1 if neg[o] else 0}>(d{o}, {name(s)}, m{o});")
-    unused = [o for o in range(4) if fuse[o] is not None]
+    unused = [o for o in range(4) if fuse[o] is not None and o not in fold_producers(circ)]
     if unused:
         lines.append("  (void)" + ", (void)".join(f"m{o}" for o in unused) + ";")
     lines.append("}")
@@ -297,10 +339,11 @@ def out_plane(half, g, o):
     return half_maps(half)[0][pinv[4 * g + o]]
 
 
-# At most this many folded positions per round: with 11 (37 key operands per round)
-# ptxas moved the round loop's index and the key loads off the uniform datapath
-# (per-thread LDC instead of LDCU), with 10 or fewer it keeps them uniform.
-FOLD_MAX_FREE = 10
+# At most this many folded positions per round.  With exactly 11 (37 key operands per
+# round, before the producer-gate folds existed) ptxas moved the round loop's index and
+# the key loads off the uniform datapath (per-thread LDC instead of LDCU); 10 and 14
+# keep them uniform (checked with tools/exp/sass_census.py after any circuit change).
+FOLD_MAX_FREE = 14
 
 
 def fold_plan(circs):
@@ -312,7 +355,8 @@ def fold_plan(circs):
     Returns per half (0 = round A, 1 = round B): the unfused outputs [(g, o)], the
     plane each writes, the next-round E-position each designates, the free
     (designated) E-positions of the round, and the remaining key positions."""
-    unf = [(g, o) for g in range(8) for o in range(4) if (circs[g].get("fuse") or [None] * 4)[o] is None]
+    unf = [(g, o) for g in range(8) for o in range(4)
+           if (circs[g].get("fuse") or [None] * 4)[o] is None or o in fold_producers(circs[g])]
     unf = unf[:int(os.environ.get("TDES_GEN_MAX_FREE", FOLD_MAX_FREE))]
     plan = {}
     for x, half in enumerate("AB"):
@@ -505,6 +549,12 @@ def emit_header(circs):
         "  return I % 4 == 0 ? v.x : I % 4 == 1 ? v.y : I % 4 == 2 ? v.z : v.w;",
         "}",
         "",
+        "// LUT(a, b, m) with m a uniform mask (a folded producer gate).",
+        "template <unsigned LUT>",
+        "__device__ __forceinline__ uint32_t lop3m(uint32_t a, uint32_t b, uint32_t m) {",
+        "  return lop3<LUT>(a, b, m);",
+        "}",
+        "",
         "// d ^ t ^ m (NEG: d ^ ~t ^ m) as one LOP3; m is a uniform mask (mask folding).",
         "template <int NEG>",
         "__device__ __forceinline__ uint32_t xor3(uint32_t d, uint32_t t, uint32_t m) {",
@@ -540,6 +590,14 @@ def emit_header(circs):
         "#pragma unroll",
         "  for (int i = 0; i < W; ++i) d.w[i] = ~a.w[i];",
         "  return d;",
+        "}",
+        "",
+        "template <unsigned LUT, int W>",
+        "__device__ __forceinline__ Vec<W> lop3m(const Vec<W>& a, const Vec<W>& b, uint32_t m) {",
+        "  Vec<W> r;",
+        "#pragma unroll",
+        "  for (int i = 0; i < W; ++i) r.w[i] = lop3m<LUT>(a.w[i], b.w[i], m);",
+        "  return r;",
         "}",
         "",
         "template <int NEG, int W>",
