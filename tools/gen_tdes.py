@@ -339,11 +339,14 @@ def out_plane(half, g, o):
     return half_maps(half)[0][pinv[4 * g + o]]
 
 
-# At most this many folded positions per round.  With exactly 11 (37 key operands per
-# round, before the producer-gate folds existed) ptxas moved the round loop's index and
-# the key loads off the uniform datapath (per-thread LDC instead of LDCU); 10 and 14
-# keep them uniform (checked with tools/exp/sass_census.py after any circuit change).
-FOLD_MAX_FREE = 14
+# At most this many folded positions per round.  The count is also rounded down to
+# even: with an odd number of key operands per round (37 or 31 measured) ptxas moved
+# the round loop's index and the key loads off the uniform datapath (per-thread LDC
+# instead of LDCU); with 38, 34 and 32 it keeps them uniform (re-check with
+# tools/exp/sass_census.py after any circuit change).  (Preferring, at equal gate
+# count, the S7 circuit with 3 more foldable outputs -- 16 folds -- measured 0.5%
+# slower than the current circuits with 14.)
+FOLD_MAX_FREE = 24
 
 
 def fold_plan(circs):
@@ -358,6 +361,7 @@ def fold_plan(circs):
     unf = [(g, o) for g in range(8) for o in range(4)
            if (circs[g].get("fuse") or [None] * 4)[o] is None or o in fold_producers(circs[g])]
     unf = unf[:int(os.environ.get("TDES_GEN_MAX_FREE", FOLD_MAX_FREE))]
+    unf = unf[:len(unf) // 2 * 2]
     plan = {}
     for x, half in enumerate("AB"):
         other = "B" if half == "A" else "A"
