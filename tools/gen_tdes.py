@@ -379,6 +379,11 @@ def fold_plan(circs):
     return plan
 
 
+# Emission order of the S-boxes inside a round (ptxas's list scheduler starts from
+# source order); an experiment switch.
+SBOX_ORDER = [int(x) for x in os.environ.get("TDES_GEN_SBOX_ORDER", "0,1,2,3,4,5,6,7").split(",")]
+
+
 def emit_round(half, plan):
     dst, src = half_maps(half)
     pl = plan[half]
@@ -394,7 +399,7 @@ def emit_round(half, plan):
              "template <bool MULHI, class V, class SP, class KP, class DP>",
              f"__device__ __forceinline__ void round_{half}(V (&P)[64], const SP* __restrict__ S,",
              "                                        const KP* __restrict__ K, const DP* __restrict__ D, uint32_t c) {"]
-    for g in range(8):
+    for g in SBOX_ORDER:
         xs = []
         for i in range(6):
             pos = 6 * g + i
