@@ -14,7 +14,7 @@ import synthetic  # noqa: E402
 lib = tdes._lib
 lib.tdes_set_trace.argtypes = [ctypes.c_void_p]
 s = tdes.key_schedule(*synthetic.KEYS_3KEY)
-for e in (19, 20, 21, 22, 23):
+for e in (int(a) for a in (sys.argv[1:] or ["19", "20", "21", "22", "23"])):
     n = 1 << e
     ntiles = n // 1024
     x = torch.empty(8 * n, dtype=torch.uint8, device="cuda"); tdes.fill_splitmix64(x)
