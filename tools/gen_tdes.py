@@ -167,7 +167,10 @@ def load_searched():
             if not verify_circuit(g, circ):
                 print(f"warning: {path} S{g + 1} circuit fails verification; ignored", file=sys.stderr)
                 continue
-            if g not in best or circuit_cost(circ) < circuit_cost(best[g]):
+            prefer = os.environ.get("TDES_GEN_PREFER", "")  # experiment: "S:file.json,..." wins ties
+            preferred = f"{g + 1}:{os.path.basename(path)}" in prefer.split(",")
+            if g not in best or circuit_cost(circ) < circuit_cost(best[g]) or (
+                    preferred and circuit_cost(circ) == circuit_cost(best[g])):
                 best[g] = circ
     return best
 
