@@ -236,3 +236,28 @@ def test_kernel_structure_with_folded_masks_matches_oracle(gen, keys, decrypt):
     p = synthetic.plaintext_bytes(0, 32 * 8)
     got = emulate_kernel(circs, p, ops)
     assert np.array_equal(got, oracle.tdes_ecb(*keys, p, decrypt=decrypt))
+
+
+def test_producer_gate_mask_folding_is_exact(gen):
+    """The generator's masked producer gates (LUT(a, b) ^ m in the gate's free input)
+    flip exactly their fused output when m = all-ones, and change nothing when m = 0:
+    exhaustive over the 64 S-box inputs, for every folded producer."""
+    _, circs = gen
+    n_checked = 0
+    for g, c in enumerate(circs):
+        for o, k in gen_tdes.fold_producers(c).items():
+            a, b, mlut = gen_tdes.masked_lut(c["gates"][k])
+            for m in (0, gen_tdes.FULL):
+                gates = list(c["gates"])
+                sig = list(gen_tdes.VARS)
+                for i, (lut, x, y, z) in enumerate(gates):
+                    if i == k:
+                        sig.append(gen_tdes.lut_eval(mlut, sig[a], sig[b], m))
+                    else:
+                        sig.append(gen_tdes.lut_eval(lut, sig[x], sig[y], sig[z]))
+                fu, fv, h = c["fuse"][o]
+                got = gen_tdes.fused_eval(h, sig[fu], sig[fv])
+                exp = gen_tdes.sbox_tt(g, o) ^ m
+                assert got == exp, (g, o, m)
+            n_checked += 1
+    assert n_checked == sum(len(gen_tdes.fold_producers(c)) for c in circs)
