@@ -9,10 +9,19 @@ fused kernel launch: load, transpose, 48 rounds, transpose, store) over the
 flush is needed between steps.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--workload c2|c4|c5] [--gather]
 
-N > 1 runs under torchrun, one process per GPU, each rank encrypting its own
-1 GiB block-range shard of the global data (weak scaling, no collective on the
-data path; NCCL only for the barrier and the max-over-ranks time).
+N > 1 runs one process per GPU: under torchrun (WORLD_SIZE set, which must equal
+--gpus) or, when started as plain `python bench.py --gpus N`, by re-launching
+itself under torch.distributed.run with N ranks.  Each rank encrypts its own
+block-range shard of the global data (c2: 1 GiB per GPU, weak scaling; c4/c5: a
+fixed total, strong scaling); there is no collective on the data path, NCCL
+carries only the barrier, the max-over-ranks time and 8-byte digests.
+
+The line's `check` compares the ciphertext's sum64 digest (summed over ranks)
+with OpenSSL's for the same global block range (tests/golden/digests.json,
+tests/helpers/make_digests.py) and counts blocks where decrypt(encrypt(x)) != x; the
+process exits 1 if either check fails.
 
 ``--impl reference`` times the CPU oracle (oracle/, the literal char-per-bit
 C implementation, OpenMP over blocks as in the paper's CPU baseline)
@@ -72,6 +81,18 @@ def read_peaks():
             return json.load(f), "measured"
     except (OSError, ValueError):
         return {"hbm_gbs": HBM_PEAK_FALLBACK, "sm_max_mhz": 1965.0}, "fallback"
+
+
+def read_counters():
+    """ALU-pipe instruction counts of the kernel from the committed ncu capture, if any
+    (profiles/kernel_counters.json, written by tools/summarize_ncu.py)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "kernel_counters.json")) as f:
+            d = json.load(f)
+        float(d["alu_thread_inst_per_block"])
+        return d
+    except (OSError, ValueError, KeyError, TypeError):
+        return None
 
 
 def read_traffic():
@@ -239,13 +260,196 @@ def run_reference(args, rank, world):
 
 # ----------------------------------------------------------------- our arm --
 
+GOLDEN_DIGESTS = os.path.join(ROOT, "tests", "golden", "digests.json")
+
+
+def expected_sum64(first: int, nblocks: int, path: str = GOLDEN_DIGESTS):
+    """Expected 3-key encrypt sum64 of global blocks [first, first+nblocks), or None.
+
+    From tests/golden/digests.json, written by tests/helpers/make_digests.py with OpenSSL
+    (pyca cryptography) only: per-1-GiB-segment sums (c2 at any N, c4, c5) and
+    whole-prefix sums (C1 and the C2 sweep sizes)."""
+    try:
+        with open(path) as f:
+            g = json.load(f)
+    except (OSError, ValueError):
+        return None
+    seg = int(g["segment_blocks"])
+    if first % seg == 0 and nblocks % seg == 0 and (first + nblocks) // seg <= len(g["enc3_seg_sum64"]):
+        s = sum(int(v, 16) for v in g["enc3_seg_sum64"][first // seg:(first + nblocks) // seg])
+        return s & ((1 << 64) - 1)
+    p = g["prefix"].get(f"enc_3key_{nblocks}")
+    if first == 0 and p is not None:
+        return int(p["sum64"], 16)
+    return None
+
+
+class CudaOps:
+    """The product path on this rank's GPU: device buffers, the C-ABI kernels, CUDA events.
+
+    bench.rank_loop() only talks to this interface, so the multi-rank host logic
+    runs unchanged in the CPU tests (tests/test_multi_rank.py) with a stub."""
+
+    def __init__(self, local_rank: int):
+        import torch
+        import paper_2007_10752_b200 as tdes
+        self.torch, self.tdes = torch, tdes
+        torch.cuda.set_device(local_rank)
+        self.dev = torch.device("cuda", local_rank)
+        self.stream = torch.cuda.current_stream(self.dev)
+        self.handle = self.stream.cuda_stream
+
+    def free_bytes(self) -> int:
+        return self.torch.cuda.mem_get_info(self.dev)[0]
+
+    def schedule(self, keys):
+        return self.tdes.key_schedule(*keys)
+
+    def plaintext(self, first: int, n: int):
+        """Device buffers (x = synthetic plaintext of global blocks [first, first+n), y)."""
+        x = self.torch.empty(8 * n, dtype=self.torch.uint8, device=self.dev)
+        self.tdes.fill_splitmix64(x, first_index=first)
+        return x, self.torch.empty_like(x)
+
+    def encrypt(self, sched, x, y, n):
+        self.tdes.ecb_encrypt_ptr(sched, x.data_ptr(), y.data_ptr(), n, self.handle)
+
+    def decrypt(self, sched, x, y, n):
+        self.tdes.ecb_decrypt_ptr(sched, x.data_ptr(), y.data_ptr(), n, self.handle)
+
+    def sum64(self, y) -> int:
+        return self.tdes.sum64(y)
+
+    def mismatch(self, a, b) -> int:
+        return self.tdes.count_mismatch(a, b)
+
+    def event(self):
+        return self.torch.cuda.Event(enable_timing=True)
+
+    def record(self, ev):
+        ev.record(self.stream)
+
+    @staticmethod
+    def elapsed_ms(a, b) -> float:
+        return a.elapsed_time(b)
+
+    def sync(self):
+        self.torch.cuda.synchronize(self.dev)
+
+
+def step_launches(ops, wl, sched, x, y, n):
+    """One step: one fused launch (c2, c4) or encrypt + in-place decrypt (c5)."""
+    yield lambda: ops.encrypt(sched, x, y, n)
+    if wl["roundtrip"]:
+        yield lambda: ops.decrypt(sched, y, y, n)
+
+
+def rank_loop(ops, workload: str, rank: int, world: int, steps: int, warmup: int,
+              barrier=lambda: None, sampler=None, per_gpu=None, gather=False):
+    """Everything one rank does for the device-timed line (the driver's contract).
+
+    Shards the workload's global block range (ECB; no collective on
+    the data path), runs `warmup` untimed steps, then exactly `steps` timed steps
+    bracketed by barrier + synchronize with events on the launching stream, and
+    reduces max time / mismatches / digests over ranks.  Returns a dict; `value`
+    etc. are the whole-job figures, identical on every rank."""
+    from paper_2007_10752_b200 import shard
+    wl = WORKLOADS[workload]
+    if per_gpu is None:
+        per_gpu = wl["per_gpu"]
+    total = wl["total"] if wl["total"] is not None else per_gpu * world
+    lo, hi = shard.shard_range(total, world, rank)
+    n = hi - lo
+    if 16 * n + (1 << 30) > ops.free_bytes():
+        raise SystemExit(f"workload {workload}: {16 * n / 2**30:.0f} GiB of buffers per GPU "
+                         f"do not fit in {ops.free_bytes() / 2**30:.0f} GiB free; use more GPUs")
+    sched = ops.schedule(synthetic.KEYS_3KEY)
+    x, y = ops.plaintext(lo, n)
+    for _ in range(warmup):
+        for launch in step_launches(ops, wl, sched, x, y, n):
+            launch()
+    ops.sync()
+
+    lps = 2 if wl["roundtrip"] else 1
+    starts = [ops.event() for _ in range(steps * lps)]
+    ends = [ops.event() for _ in range(steps * lps)]
+    t_begin, t_end = ops.event(), ops.event()
+    barrier()
+    ops.sync()
+    with (sampler if sampler is not None else _NullCtx()):
+        ops.record(t_begin)
+        k = 0
+        for _ in range(steps):
+            for launch in step_launches(ops, wl, sched, x, y, n):
+                ops.record(starts[k])
+                launch()
+                ops.record(ends[k])
+                k += 1
+        ops.record(t_end)
+        ops.sync()
+    barrier()
+    local_ms = ops.elapsed_ms(t_begin, t_end)
+    kern_ms = [ops.elapsed_ms(s, e) for s, e in zip(starts, ends)]
+    elapsed_ms = shard.max_over_ranks(local_ms)
+
+    # ---- correctness of this run: dec(enc(x)) == x on every block, and the
+    #      ciphertext digest against OpenSSL's (tests/golden/digests.json) ----
+    if wl["roundtrip"]:
+        mismatch = ops.mismatch(y, x)              # y = dec(enc(x)) after the last step
+        ops.encrypt(sched, x, y, n)
+        digest = ops.sum64(y)
+    else:
+        digest = ops.sum64(y)
+    res_gather = None
+    if gather and world > 1 and not wl["roundtrip"]:
+        # optional NVLink gather of the ciphertext to rank 0 (north_star); not in the timed step
+        g0, g1 = ops.event(), ops.event()
+        barrier()
+        ops.sync()
+        ops.record(g0)
+        full = shard.gather_shards(y, total, dst=0)
+        ops.record(g1)
+        ops.sync()
+        gms = shard.max_over_ranks(ops.elapsed_ms(g0, g1))
+        res_gather = {"ms": gms, "bytes": 8 * total, "GB_per_s": 8 * total / (gms * 1e-3) / 1e9,
+                      "how": "torch.distributed gather of every rank's ciphertext shard into one buffer on rank 0"}
+        if rank == 0:
+            res_gather["sum64_ok"] = ops.sum64(full) == shard.sum_u64_over_ranks(digest)
+        else:
+            shard.sum_u64_over_ranks(digest)
+        del full
+    if not wl["roundtrip"]:
+        ops.decrypt(sched, y, y, n)
+        mismatch = ops.mismatch(y, x)
+    mismatch = shard.sum_over_ranks(mismatch)
+    digest = shard.sum_u64_over_ranks(digest)
+    expected = expected_sum64(0, total)
+    lo_hi = shard.all_gather_ints([lo, hi])
+    return {"workload": workload, "wl": wl, "total": total, "n": n, "lo": lo, "hi": hi, "shards": lo_hi,
+            "sched": sched, "x": x, "y": y,
+            "steps": steps, "launches_per_step": lps, "elapsed_ms": elapsed_ms, "local_ms": local_ms,
+            "kern_ms": kern_ms, "value": steps * total * 8 / (elapsed_ms * 1e-3) / 1e9,
+            "mismatch": mismatch, "digest": digest, "digest_expected": expected,
+            "digest_ok": (digest == expected) if expected is not None else None,
+            "gather": res_gather}
+
+
+class _NullCtx:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
     import paper_2007_10752_b200 as tdes
+    from paper_2007_10752_b200 import shard
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    ops = CudaOps(local_rank)
+    dev = ops.dev
     distributed = world > 1 or "TORCHELASTIC_RUN_ID" in os.environ  # torchrun: exercise NCCL even at N=1
     if distributed:
         dist.init_process_group("nccl", device_id=dev)
@@ -254,23 +458,7 @@ def run_ours(args, rank, world, local_rank):
         if distributed:
             dist.barrier()
 
-    from paper_2007_10752_b200 import shard
-    wl = WORKLOADS[args.workload]
-    total_blocks = wl["total"] if wl["total"] is not None else wl["per_gpu"] * world
-    lo, hi = shard.shard_range(total_blocks, world, rank)
-    n = hi - lo
-    free_b, _ = torch.cuda.mem_get_info(dev)
-    if 16 * n + (1 << 30) > free_b:
-        raise SystemExit(f"workload {args.workload}: {16 * n / 2**30:.0f} GiB of buffers per GPU "
-                         f"do not fit in {free_b / 2**30:.0f} GiB free; use more GPUs")
-    launches_per_step = 2 if wl["roundtrip"] else 1
-    sched = tdes.key_schedule(*synthetic.KEYS_3KEY)
-    x = torch.empty(8 * n, dtype=torch.uint8, device=dev)
-    y = torch.empty_like(x)
-    tdes.fill_splitmix64(x, first_index=lo)
-    stream = torch.cuda.current_stream(dev)
-    handle = stream.cuda_stream
-
+    stream = ops.stream
     # ---- LOP3 peak microbenchmark (roofline cross-check, same process) ----
     sms, occ = tdes.device_geometry()
     sink = torch.empty(sms * 8 * 256, dtype=torch.int32, device=dev)
@@ -278,68 +466,32 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
-    ops = tdes.lop3_peak_launch(sink, sms * 8, 256, 8192)
+    ops_count = tdes.lop3_peak_launch(sink, sms * 8, 256, 8192)
     ev1.record(stream)
     ev1.synchronize()
-    lop3_peak_meas = ops / (ev0.elapsed_time(ev1) * 1e-3) / 1e12   # Tops/s
+    lop3_peak_meas = ops_count / (ev0.elapsed_time(ev1) * 1e-3) / 1e12   # Tops/s
+    del sink
 
-    def step_launches():
-        """One step: one fused launch (c2, c4) or encrypt + in-place decrypt (c5)."""
-        yield lambda: tdes.ecb_encrypt_ptr(sched, x.data_ptr(), y.data_ptr(), n, handle)
-        if wl["roundtrip"]:
-            yield lambda: tdes.ecb_decrypt_ptr(sched, y.data_ptr(), y.data_ptr(), n, handle)
-
-    # ---- warmup ----
-    for _ in range(args.warmup):
-        for launch in step_launches():
-            launch()
-    torch.cuda.synchronize()
-
-    # ---- timed region: K steps ----
-    nl = args.steps * launches_per_step
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(nl)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(nl)]
-    t_begin, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     props = torch.cuda.get_device_properties(dev)
     bus = None
     if hasattr(props, "pci_bus_id"):
         bus = f"{getattr(props, 'pci_domain_id', 0):04x}:{props.pci_bus_id:02x}:{getattr(props, 'pci_device_id', 0):02x}.0"
     sampler = ClockSampler(bus, local_rank)
-    barrier()
-    torch.cuda.synchronize()
-    with sampler:
-        t_begin.record(stream)
-        k = 0
-        for _ in range(args.steps):
-            for launch in step_launches():
-                starts[k].record(stream)
-                launch()
-                ends[k].record(stream)
-                k += 1
-        t_end.record(stream)
-        torch.cuda.synchronize()
-    barrier()
-    elapsed_ms = t_begin.elapsed_time(t_end)
-    kern_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    elapsed_ms = shard.max_over_ranks(elapsed_ms)
+    r = rank_loop(ops, args.workload, rank, world, args.steps, args.warmup, barrier=barrier, sampler=sampler,
+                  gather=args.gather)
+    wl, n, total, sched = r["wl"], r["n"], r["total"], r["sched"]
+    kern_ms, elapsed_ms, lps = r["kern_ms"], r["elapsed_ms"], r["launches_per_step"]
     clocks = sampler.summary()
-
-    # ---- device-side sanity: decrypt restores the plaintext; digest ----
-    if wl["roundtrip"]:
-        mismatch = tdes.count_mismatch(y, x)       # y = dec(enc(x)) after the last step
-        tdes.ecb_encrypt_ptr(sched, x.data_ptr(), y.data_ptr(), n, handle)
-        digest = tdes.sum64(y)
-    else:
-        digest = tdes.sum64(y)
-        tdes.ecb_decrypt_ptr(sched, y.data_ptr(), y.data_ptr(), n, handle)
-        mismatch = tdes.count_mismatch(y, x)
-    mismatch = shard.sum_over_ranks(mismatch)
-    digest = shard.sum_u64_over_ranks(digest)
+    if distributed:
+        reasons = [None] * world
+        dist.all_gather_object(reasons, clocks.get("reasons", []))
+        clocks["reasons_all_ranks"] = sorted({x for rs in reasons for x in rs})
 
     # ---- e2e: same metric through the host-buffer C-ABI call ----
     # (a bounded prefix of the shard for c4/c5: at most 1 GiB of pinned host memory per direction)
     ne = min(n, E2E_MAX_BLOCKS)
-    del y
+    x = r.pop("x")
+    r.pop("y")
     torch.cuda.empty_cache()
     hin = torch.empty(8 * ne, dtype=torch.uint8).pin_memory()
     hin.copy_(x[:8 * ne].cpu())
@@ -361,8 +513,7 @@ def run_ours(args, rank, world, local_rank):
             stream.wait_stream(s)
     e1.record(stream)
     e1.synchronize()
-    e2e_ms = e0.elapsed_time(e1)
-    e2e_ms = shard.max_over_ranks(e2e_ms)
+    e2e_ms = shard.max_over_ranks(e0.elapsed_time(e1))
     e2e_value = e2e_steps * ne * world * 8 / (e2e_ms * 1e-3) / 1e9
 
     if rank == 0:
@@ -379,44 +530,61 @@ def run_ours(args, rank, world, local_rank):
         sm_max = float(peaks.get("sm_max_mhz", 1965.0))
         peak = sms * LOP3_LANES_PER_SM * sm_max * 1e6 / 1e12
         tb, tsrc = read_traffic()
-        value = args.steps * total_blocks * 8 / (elapsed_ms * 1e-3) / 1e9
+        counters = read_counters()
+        value = r["value"]
         hbm_gbs = 16 * n / avg_kern_s / 1e9
+        roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tops/s",
+                    "frac": achieved / peak,
+                    "traffic": (tb * n if tb is not None else None),
+                    "ops_per_block": g_alg, "sbox_lop3_total": T,
+                    "ops_per_block_incl_key_xor": g_alg_kx,
+                    "frac_incl_key_xor": g_alg_kx * n / avg_kern_s / 1e12 / peak,
+                    "peak_basis": f"{sms} SMs x {LOP3_LANES_PER_SM} LOP3 lanes/clk x {sm_max:.0f} MHz (sm_max_mhz, {peaks_src})",
+                    "peak_microbench": lop3_peak_meas,
+                    "frac_of_microbench": achieved / lop3_peak_meas,
+                    "kernel_ms_avg": avg_kern_s * 1e3,
+                    "kernel_ms_p10_p50_p90": [round(float(np.percentile(kern_ms, q)), 5) for q in (10, 50, 90)],
+                    "hbm": {"achieved_gbs": hbm_gbs, "peak_gbs": float(peaks.get("hbm_gbs", HBM_PEAK_FALLBACK)),
+                            "frac": hbm_gbs / float(peaks.get("hbm_gbs", HBM_PEAK_FALLBACK)),
+                            "bytes_per_block": 16, "peak_source": peaks_src},
+                    "traffic_source": tsrc}
+        if counters is not None:
+            # every ALU-pipe instruction the kernel issues (S-box gates, Feistel XORs,
+            # transposes, loop control), counted by ncu on the committed capture
+            ipb = counters["alu_thread_inst_per_block"]
+            roofline["alu_inst_per_block"] = ipb
+            roofline["alu_inst_frac"] = ipb * n / avg_kern_s / 1e12 / peak
+            roofline["alu_pipe_util_ncu"] = counters.get("alu_pipe_pct")
+            roofline["counters_source"] = counters.get("source")
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
             "scaling": wl["scaling"], "vs_baseline": None, "dtype": "u32", "data": "synthetic",
             "config": {"workload": wl["desc"], "name": args.workload, "blocks_per_gpu": n,
-                       "bytes_per_gpu": n * 8, "total_blocks": total_blocks,
+                       "bytes_per_gpu": n * 8, "total_blocks": total,
                        "op": "encrypt+decrypt" if wl["roundtrip"] else "encrypt", "keys": "3-key",
                        "parallelism": f"dp{world} (block-range shards)",
                        "l2": f"inputs and outputs {n * 8 / 2**30:.2f} GiB per GPU > 126 MB L2; no flush needed",
                        "Gblocks_per_s": value / 8},
-            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tops/s",
-                         "frac": achieved / peak,
-                         "traffic": (tb * n if tb is not None else None),
-                         "ops_per_block": g_alg, "sbox_lop3_total": T,
-                         "ops_per_block_incl_key_xor": g_alg_kx,
-                         "frac_incl_key_xor": g_alg_kx * n / avg_kern_s / 1e12 / peak,
-                         "peak_basis": f"{sms} SMs x {LOP3_LANES_PER_SM} LOP3 lanes/clk x {sm_max:.0f} MHz (sm_max_mhz, {peaks_src})",
-                         "peak_microbench": lop3_peak_meas,
-                         "frac_of_microbench": achieved / lop3_peak_meas,
-                         "kernel_ms_avg": avg_kern_s * 1e3,
-                         "kernel_ms_p10_p50_p90": [round(float(np.percentile(kern_ms, q)), 5) for q in (10, 50, 90)],
-                         "hbm": {"achieved_gbs": hbm_gbs, "peak_gbs": float(peaks.get("hbm_gbs", HBM_PEAK_FALLBACK)),
-                                 "frac": hbm_gbs / float(peaks.get("hbm_gbs", HBM_PEAK_FALLBACK)),
-                                 "bytes_per_block": 16, "peak_source": peaks_src},
-                         "traffic_source": tsrc},
+            "roofline": roofline,
             "clocks": clocks,
             "e2e": {"value": e2e_value, "unit": UNIT,
-                    "h2d_bytes_per_step": 8 * ne * launches_per_step,
-                    "d2h_bytes_per_step": 8 * ne * launches_per_step,
+                    "h2d_bytes_per_step": 8 * ne * lps,
+                    "d2h_bytes_per_step": 8 * ne * lps,
                     "how": "tdes_ecb_crypt_host: pinned host in/out, 32 MiB chunks on 3 streams (H2D, kernel, D2H overlapped)"
                            + ("" if ne == n else f"; first {ne} blocks of each shard")
                            + ("; encrypt then decrypt in place" if wl["roundtrip"] else ""),
                     "steps": e2e_steps},
-            "gpu_launches": nl,
-            "check": {"device_roundtrip_mismatch_blocks": mismatch, "ciphertext_sum64": f"{digest:016x}"},
+            "gpu_launches": args.steps * lps * world,
+            "check": {"device_roundtrip_mismatch_blocks": r["mismatch"],
+                      "ciphertext_sum64": f"{r['digest']:016x}",
+                      "expected_sum64": (f"{r['digest_expected']:016x}" if r["digest_expected"] is not None else None),
+                      "digest_ok": r["digest_ok"],
+                      "expected_source": "tests/golden/digests.json (OpenSSL via pyca, tests/helpers/make_digests.py)",
+                      "shards": r["shards"]},
         }
+        if r["gather"] is not None:
+            line["gather"] = r["gather"]
         if world == 1 and not args.no_cpu_baseline and args.workload == "c2":
             v, used, sample, secs = oracle_rate(args.cpu_seconds, BLOCKS_PER_GPU)
             line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": used, "kind": "oracle",
@@ -425,7 +593,36 @@ def run_ours(args, rank, world, local_rank):
     if distributed:
         dist.barrier()
         dist.destroy_process_group()
+    if r["digest_ok"] is False or r["mismatch"] != 0:
+        print(f"bench: output check FAILED (digest_ok={r['digest_ok']}, mismatch={r['mismatch']})", file=sys.stderr)
+        return 1
     return 0
+
+
+def _free_port() -> int:
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def relaunch_cmd(argv, nproc: int, port: int) -> list:
+    """torchrun command that re-runs this script with the same arguments, one rank per GPU."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *argv]
+
+
+def relaunch(args, argv) -> int:
+    """`python bench.py --gpus N` without torchrun: start N ranks (one per GPU) under
+    torch.distributed.run; rank 0's JSON line reaches our stdout."""
+    import subprocess
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(f"bench: --gpus {args.gpus} needs {args.gpus} visible GPUs, found {have}", file=sys.stderr)
+        return 2
+    res = subprocess.run(relaunch_cmd(argv, args.gpus, _free_port()), stdout=JSON_OUT.fileno())
+    return res.returncode
 
 
 def _json_stdout():
@@ -444,8 +641,9 @@ def emit(line: dict):
 JSON_OUT = sys.stdout
 
 
-def main():
+def main(argv=None):
     global JSON_OUT
+    argv = sys.argv[1:] if argv is None else argv
     JSON_OUT = _json_stdout()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -454,17 +652,28 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--gather", action="store_true",
+                    help="N > 1: also time gathering every rank's ciphertext on rank 0 (NCCL), outside the step")
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS),
                     help="c2: 1 GiB encrypt per GPU (default, weak scaling); c4: 8 GiB total encrypt; "
                          "c5: 64 GiB total encrypt+decrypt round trip (strong scaling)")
-    args = ap.parse_args()
+    args = ap.parse_args(argv)
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    launched = "WORLD_SIZE" in os.environ
     rank = env_int("RANK", 0)
     world = env_int("WORLD_SIZE", 1)
     local_rank = env_int("LOCAL_RANK", 0)
     if args.impl == "reference":
+        # the oracle runs on rank 0 only; other ranks exit without work
         return run_reference(args, rank, world)
+    if not launched and args.gpus > 1:
+        return relaunch(args, argv)
+    if world != args.gpus:
+        print(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}; launch one rank per GPU", file=sys.stderr)
+        return 2
     return run_ours(args, rank, world, local_rank)
 
 

@@ -37,7 +37,9 @@ extern "C" {
 typedef struct CUstream_st *tdes_stream_t;
 
 #define TDES_OK 0
-#define TDES_ERR_INVALID_ARG (-1) /* NULL schedule/key/pointer with nblocks > 0, bad enum */
+#define TDES_ERR_INVALID_ARG (-1) /* NULL schedule/key/pointer with nblocks > 0, bad enum,
+                                     nblocks > SIZE_MAX/16; TDES_DEBUG builds also: in/out
+                                     not device memory of the current device            */
 #define TDES_ERR_MISALIGNED (-2)  /* in or out not 8-byte aligned                        */
 #define TDES_ERR_OVERLAP (-3)     /* in and out partially overlap (in == out is allowed)  */
 #define TDES_ERR_CUDA (-4)        /* a CUDA call failed; see tdes_last_cuda_error()       */
@@ -81,6 +83,16 @@ int tdes_key_schedule(const uint8_t k1[8], const uint8_t k2[8], const uint8_t k3
  *           alignment of both selects 128-bit loads/stores.
  *   nblocks number of 8-byte blocks; 0 returns TDES_OK without a launch.
  * The library allocates nothing and never synchronizes.
+ * Errors (checked in this order, nothing is launched on an error):
+ *   TDES_ERR_INVALID_ARG  s, in or out NULL (nblocks > 0), nblocks > SIZE_MAX/16;
+ *                         in a TDES_DEBUG build (libtdes_b200_debug.so) also in or
+ *                         out not device (or managed) memory of the current device
+ *                         per cudaPointerGetAttributes -- release builds do not
+ *                         make that driver call and a host pointer faults in the
+ *                         kernel instead (reported at the next synchronize);
+ *   TDES_ERR_MISALIGNED   in or out not 8-byte aligned;
+ *   TDES_ERR_OVERLAP      in != out and the ranges overlap;
+ *   TDES_ERR_CUDA         cudaGetDevice or the launch failed (tdes_last_cuda_error). 
  */
 int tdes_ecb_encrypt(const tdes_schedule *s, const void *in, void *out, size_t nblocks,
                      tdes_stream_t stream);
@@ -138,7 +150,8 @@ int tdes_get_kernel_info(tdes_kernel_info *out);
 /* Human-readable text of a TDES_ERR_* code (static storage). */
 const char *tdes_strerror(int code);
 
-/* cudaError_t of the last TDES_ERR_CUDA returned on this host thread. */
+/* cudaError_t of the last TDES_ERR_CUDA returned on this host thread by any
+ * entry point of the library (tdes.h, tdes_bench.h, tdes_paper.h); 0 if none. */
 int tdes_last_cuda_error(void);
 
 #ifdef __cplusplus

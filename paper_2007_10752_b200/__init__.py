@@ -143,9 +143,16 @@ def subkeys(s: TdesSchedule) -> list[list[int]]:
     return [[int(s.subkey[k][r]) for r in range(16)] for k in range(3)]
 
 
-def _stream_handle(stream) -> int:
-    st = stream if stream is not None else torch.cuda.current_stream()
-    return int(st.cuda_stream)
+def _stream_handle(stream, device=None) -> int:
+    """The raw handle of `stream` (default: the current stream of `device`).
+
+    The C ABI launches on the *current* device, so every call below runs inside
+    ``torch.cuda.device(x.device)``; an explicit stream must live on that device."""
+    if stream is None:
+        return int(torch.cuda.current_stream(device).cuda_stream)
+    if device is not None and stream.device != torch.device(device):
+        raise ValueError(f"stream is on {stream.device}, the tensors on {device}")
+    return int(stream.cuda_stream)
 
 
 def _prep(x: torch.Tensor, out):
@@ -157,13 +164,16 @@ def _prep(x: torch.Tensor, out):
         out = torch.empty_like(x)
     if not (out.is_cuda and out.is_contiguous() and out.dtype == torch.uint8 and out.numel() == x.numel()):
         raise ValueError("out must be a contiguous uint8 CUDA tensor of the input's size")
+    if out.device != x.device:
+        raise ValueError(f"out is on {out.device}, the input on {x.device}")
     return out
 
 
 def _crypt(fn, sched, x, out, stream, what):
     out = _prep(x, out)
-    _check(fn(ctypes.byref(sched), x.data_ptr(), out.data_ptr(), x.numel() // 8,
-              _stream_handle(stream)), what)
+    with torch.cuda.device(x.device):
+        _check(fn(ctypes.byref(sched), x.data_ptr(), out.data_ptr(), x.numel() // 8,
+                  _stream_handle(stream, x.device)), what)
     return out
 
 
@@ -188,8 +198,10 @@ def des_ecb_decrypt(x, sched: DesSchedule, out=None, stream=None):
 def ecb_crypt_mode(x: torch.Tensor, sched: TdesSchedule, mode: int, decrypt=False, out=None, stream=None):
     """3DES ECB with an explicit kernel choice (MODE_AUTO / MODE_THROUGHPUT / MODE_SPLIT)."""
     out = _prep(x, out)
-    _check(_lib.tdes_ecb_crypt_mode(ctypes.byref(sched), int(bool(decrypt)), x.data_ptr(), out.data_ptr(),
-                                    x.numel() // 8, mode, _stream_handle(stream)), "tdes_ecb_crypt_mode")
+    with torch.cuda.device(x.device):
+        _check(_lib.tdes_ecb_crypt_mode(ctypes.byref(sched), int(bool(decrypt)), x.data_ptr(), out.data_ptr(),
+                                        x.numel() // 8, mode, _stream_handle(stream, x.device)),
+               "tdes_ecb_crypt_mode")
     return out
 
 
@@ -220,15 +232,16 @@ class HostPipeline:
                 raise ValueError("host buffers must be contiguous uint8 CPU tensors")
         if host_in.numel() % 8 or host_out.numel() != host_in.numel():
             raise ValueError("size mismatch or not a whole number of blocks")
-        # order the caller's current stream before ours (inputs may be produced on it)
-        cur = torch.cuda.current_stream(self.device)
-        for s in self.streams:
-            s.wait_stream(cur)
-        _check(_lib.tdes_ecb_crypt_host(ctypes.byref(sched), int(bool(decrypt)), host_in.data_ptr(),
-                                        host_out.data_ptr(), host_in.numel() // 8,
-                                        self.workspace.data_ptr(), self.workspace.numel(),
-                                        self.chunk_blocks, self._handles, len(self.streams)),
-               "tdes_ecb_crypt_host")
+        with torch.cuda.device(self.device):   # the C ABI launches on the current device
+            # order the caller's current stream before ours (inputs may be produced on it)
+            cur = torch.cuda.current_stream(self.device)
+            for s in self.streams:
+                s.wait_stream(cur)
+            _check(_lib.tdes_ecb_crypt_host(ctypes.byref(sched), int(bool(decrypt)), host_in.data_ptr(),
+                                            host_out.data_ptr(), host_in.numel() // 8,
+                                            self.workspace.data_ptr(), self.workspace.numel(),
+                                            self.chunk_blocks, self._handles, len(self.streams)),
+                   "tdes_ecb_crypt_host")
         return host_out
 
 
@@ -281,9 +294,12 @@ class PaperBaseline:
 
     def run(self, x: torch.Tensor, decrypt=False, out=None, stream=None):
         out = _prep(x, out)
-        _check(_lib.tdes_paper_ecb(self.keys.data_ptr(), x.data_ptr(), out.data_ptr(), x.numel() // 8,
-                                   int(bool(decrypt)), self.workspace.data_ptr(), self.workspace.numel(),
-                                   _stream_handle(stream)), "tdes_paper_ecb")
+        if x.device != self.keys.device:
+            raise ValueError(f"input on {x.device}, PaperBaseline built for {self.keys.device}")
+        with torch.cuda.device(x.device):
+            _check(_lib.tdes_paper_ecb(self.keys.data_ptr(), x.data_ptr(), out.data_ptr(), x.numel() // 8,
+                                       int(bool(decrypt)), self.workspace.data_ptr(), self.workspace.numel(),
+                                       _stream_handle(stream, x.device)), "tdes_paper_ecb")
         return out
 
 
@@ -291,28 +307,39 @@ class PaperBaseline:
 
 def fill_splitmix64(x: torch.Tensor, first_index: int = 0, seed: int = 20071075, stream=None):
     """Synthetic plaintext (DESIGN.md input recipe) generated on the device."""
-    assert x.is_cuda and x.is_contiguous() and x.numel() % 8 == 0
-    _check(_lib.tdes_fill_splitmix64(x.data_ptr(), x.numel() // 8, first_index, seed,
-                                     _stream_handle(stream)), "tdes_fill_splitmix64")
+    if not (x.is_cuda and x.is_contiguous() and x.numel() % 8 == 0):
+        raise ValueError("x must be a contiguous CUDA tensor of whole 8-byte blocks")
+    with torch.cuda.device(x.device):
+        _check(_lib.tdes_fill_splitmix64(x.data_ptr(), x.numel() // 8, first_index, seed,
+                                         _stream_handle(stream, x.device)), "tdes_fill_splitmix64")
     return x
 
 
 def sum64(x: torch.Tensor, stream=None) -> int:
     """Sum of the little-endian uint64 blocks mod 2^64 (synchronizes)."""
-    res = torch.zeros(1, dtype=torch.int64, device=x.device)
-    _check(_lib.tdes_sum64(x.data_ptr(), x.numel() // 8, res.data_ptr(), _stream_handle(stream)), "tdes_sum64")
+    if not (x.is_cuda and x.is_contiguous()):
+        raise ValueError("x must be a contiguous CUDA tensor")
+    with torch.cuda.device(x.device):
+        res = torch.zeros(1, dtype=torch.int64, device=x.device)
+        _check(_lib.tdes_sum64(x.data_ptr(), x.numel() // 8, res.data_ptr(), _stream_handle(stream, x.device)),
+               "tdes_sum64")
     return int(res.item()) & ((1 << 64) - 1)
 
 
 def count_mismatch(a: torch.Tensor, b: torch.Tensor, stream=None) -> int:
-    res = torch.zeros(1, dtype=torch.int64, device=a.device)
-    _check(_lib.tdes_count_mismatch(a.data_ptr(), b.data_ptr(), a.numel() // 8, res.data_ptr(),
-                                    _stream_handle(stream)), "tdes_count_mismatch")
+    if not (a.is_cuda and a.is_contiguous() and b.is_contiguous()) or a.device != b.device \
+            or a.numel() != b.numel():
+        raise ValueError("a and b must be contiguous CUDA tensors of one size on one device")
+    with torch.cuda.device(a.device):
+        res = torch.zeros(1, dtype=torch.int64, device=a.device)
+        _check(_lib.tdes_count_mismatch(a.data_ptr(), b.data_ptr(), a.numel() // 8, res.data_ptr(),
+                                        _stream_handle(stream, a.device)), "tdes_count_mismatch")
     return int(res.item())
 
 
 def lop3_peak_launch(sink: torch.Tensor, grid: int, cta: int, iters: int, stream=None) -> int:
     ops = ctypes.c_uint64()
-    _check(_lib.tdes_lop3_peak(sink.data_ptr(), grid, cta, iters, ctypes.byref(ops),
-                               _stream_handle(stream)), "tdes_lop3_peak")
+    with torch.cuda.device(sink.device):
+        _check(_lib.tdes_lop3_peak(sink.data_ptr(), grid, cta, iters, ctypes.byref(ops),
+                                   _stream_handle(stream, sink.device)), "tdes_lop3_peak")
     return ops.value

@@ -4,15 +4,11 @@
 #include <stdint.h>
 
 #include "../../include/tdes_bench.h"
+#include "tdes_error.h"
 
 namespace {
 
-thread_local int g_bench_err = 0;
-
-int fail(cudaError_t e) {
-  g_bench_err = (int)e;
-  return TDES_ERR_CUDA;
-}
+int fail(cudaError_t e) { return tdes_internal::cuda_fail(e); }
 
 int grid_for(size_t n, int threads) {
   size_t g = (n + threads - 1) / threads;

@@ -28,6 +28,7 @@
 #include "../../include/tdes.h"
 #include "../../include/tdes_bench.h"
 #include "gen/tdes_gen.cuh"
+#include "tdes_error.h"
 
 namespace {
 
@@ -81,8 +82,6 @@ constexpr int kKeySmem = TDES_KSMEM;
 constexpr bool kTma = TDES_TMA && kWords == 1;
 constexpr int kWarps = kThreads / 32;
 constexpr unsigned kTileBytes = kTileBlocks * 8u;
-
-thread_local int g_last_cuda_error = 0;
 
 // mulhi.s32(0x7FFFFFFF, s) = (s - 1) / 2 for s = +-1 (tdes_gen::kxor with
 // MULHI, and the split kernel's k).  Passed as a kernel argument so it lives in a
@@ -675,17 +674,17 @@ int num_sms(int dev) {
   return sms;
 }
 
-int cuda_fail(cudaError_t e) {
-  g_last_cuda_error = (int)e;
-  return TDES_ERR_CUDA;
-}
+using tdes_internal::cuda_fail;
 
+// Caller guarantees nblocks <= SIZE_MAX >> 4 (so nblocks * 8 cannot wrap).
 int check_buffers(const void* in, const void* out, size_t nblocks) {
   if (!in || !out) return TDES_ERR_INVALID_ARG;
   if (((uintptr_t)in | (uintptr_t)out) & 7u) return TDES_ERR_MISALIGNED;
   const uintptr_t a = (uintptr_t)in, b = (uintptr_t)out, len = (uintptr_t)nblocks * 8u;
   if (a != b && a < b + len && b < a + len) return TDES_ERR_OVERLAP;
-  return TDES_OK;
+  int rc = tdes_internal::check_device_pointer(in);
+  if (rc == TDES_OK) rc = tdes_internal::check_device_pointer(out);
+  return rc;
 }
 
 // Auto mode: the split (latency) kernel for launches of at most this many
@@ -773,9 +772,9 @@ template <int NSTAGES>
 int launch(const uint32_t (*masks)[48], const void* in, void* out, size_t nblocks,
            cudaStream_t stream, int mode = 0) {
   if (nblocks == 0) return TDES_OK;
+  if (nblocks > (SIZE_MAX >> 4)) return TDES_ERR_INVALID_ARG;
   const int rc = check_buffers(in, out, nblocks);
   if (rc) return rc;
-  if (nblocks > (SIZE_MAX >> 4)) return TDES_ERR_INVALID_ARG;
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return cuda_fail(e);
@@ -860,20 +859,28 @@ extern "C" int tdes_ecb_crypt_host(const tdes_schedule* s, int decrypt, const vo
   if (!host_in || !host_out || !workspace) return TDES_ERR_INVALID_ARG;
   if (((uintptr_t)workspace & 15u) || (chunk_blocks & 1u)) return TDES_ERR_MISALIGNED;
   if (workspace_bytes / 8u / (size_t)nstreams < chunk_blocks) return TDES_ERR_WORKSPACE;
+  if (nblocks > (SIZE_MAX >> 4)) return TDES_ERR_INVALID_ARG;
   const uint8_t* src = static_cast<const uint8_t*>(host_in);
   uint8_t* dst = static_cast<uint8_t*>(host_out);
   const size_t chunk_bytes = chunk_blocks * 8u;
+  // On a failure part-way through, copies already queued on the other streams
+  // still read host_in / write host_out and the workspace: wait for all of them
+  // before returning, so the caller may free or reuse the buffers at once.
+  auto drain = [&](int rc) {
+    for (int i = 0; i < nstreams; ++i) (void)cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(streams[i]));
+    return rc;
+  };
   size_t c = 0;
   for (size_t off = 0; off < nblocks; off += chunk_blocks, ++c) {
     const size_t nb = nblocks - off < chunk_blocks ? nblocks - off : chunk_blocks;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(streams[c % (size_t)nstreams]);
     uint8_t* dev = static_cast<uint8_t*>(workspace) + (c % (size_t)nstreams) * chunk_bytes;
     cudaError_t e = cudaMemcpyAsync(dev, src + off * 8u, nb * 8u, cudaMemcpyHostToDevice, st);
-    if (e != cudaSuccess) return cuda_fail(e);
+    if (e != cudaSuccess) return drain(cuda_fail(e));
     const int rc = launch<3>(s->mask[decrypt], dev, dev, nb, st);
-    if (rc) return rc;
+    if (rc) return drain(rc);
     e = cudaMemcpyAsync(dst + off * 8u, dev, nb * 8u, cudaMemcpyDeviceToHost, st);
-    if (e != cudaSuccess) return cuda_fail(e);
+    if (e != cudaSuccess) return drain(cuda_fail(e));
   }
   for (int i = 0; i < nstreams; ++i) {
     const cudaError_t e = cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(streams[i]));
@@ -892,7 +899,34 @@ extern "C" int tdes_get_kernel_info(tdes_kernel_info* out) {
   return TDES_OK;
 }
 
-extern "C" int tdes_last_cuda_error(void) { return g_last_cuda_error; }
+namespace tdes_internal {
+namespace {
+thread_local int g_last_cuda_error = 0;
+}
+int cuda_fail(cudaError_t e) {
+  g_last_cuda_error = (int)e;
+  return TDES_ERR_CUDA;
+}
+int check_device_pointer(const void* p) {
+#ifdef TDES_DEBUG
+  cudaPointerAttributes a;
+  const cudaError_t e = cudaPointerGetAttributes(&a, p);
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();  // not sticky: clear it
+    return TDES_ERR_INVALID_ARG;
+  }
+  int dev = -1;
+  if (cudaGetDevice(&dev) != cudaSuccess) return TDES_ERR_INVALID_ARG;
+  if ((a.type != cudaMemoryTypeDevice && a.type != cudaMemoryTypeManaged) || a.device != dev)
+    return TDES_ERR_INVALID_ARG;
+#else
+  (void)p;
+#endif
+  return TDES_OK;
+}
+}  // namespace tdes_internal
+
+extern "C" int tdes_last_cuda_error(void) { return tdes_internal::g_last_cuda_error; }
 
 extern "C" int tdes_fold_operands(const tdes_schedule* s, int decrypt, uint32_t* out, size_t out_words,
                                   size_t* words, int* geom) {

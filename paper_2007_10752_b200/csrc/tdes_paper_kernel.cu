@@ -20,10 +20,9 @@
 #include <stdint.h>
 
 #include "../../include/tdes_paper.h"
+#include "tdes_error.h"
 
 namespace {
-
-thread_local int g_err = 0;
 
 // Tables for the device, from the generated product tables (tools/des_tables.py);
 // c_shifts is statically initialised at module load, so calls never write shared state.
@@ -95,10 +94,7 @@ __global__ void __launch_bounds__(64) paper_crypt_kernel(const uint8_t* in, uint
   }
 }
 
-int fail(cudaError_t e) {
-  g_err = (int)e;
-  return TDES_ERR_CUDA;
-}
+int fail(cudaError_t e) { return tdes_internal::cuda_fail(e); }
 
 }  // namespace
 

@@ -56,21 +56,44 @@ def sum_over_ranks(value: int) -> int:
     return int(t.item())
 
 
+def all_gather_ints(values: list[int]) -> list[list[int]]:
+    """Every rank's short list of ints (e.g. its shard bounds), in rank order."""
+    if not dist.is_initialized() or dist.get_world_size() == 1:
+        return [list(values)]
+    t = torch.tensor(values, dtype=torch.int64, device=_device_for_backend())
+    parts = [torch.empty_like(t) for _ in range(dist.get_world_size())]
+    dist.all_gather(parts, t)
+    return [[int(v) for v in p.tolist()] for p in parts]
+
+
 def gather_shards(local: torch.Tensor, nblocks_total: int, dst: int = 0):
     """Gather every rank's uint8 shard (8 bytes per block) into one buffer on ``dst``.
 
-    Shards may differ in size by one block, so each rank sends a zero-padded
-    buffer of the largest shard size; ``dst`` returns the concatenation, other
-    ranks return None.  (Optional output path; not part of the timed step.)
+    ``dst`` receives straight into views of one preallocated buffer of the largest
+    shard size per rank; when the shards differ in size (by one block) the result
+    is compacted in place.  Other ranks return None.  (Optional output path, e.g.
+    the bench's ``--gather`` leg over NCCL; not part of the timed step.)
     """
     world = dist.get_world_size()
     rank = dist.get_rank()
     sizes = [shard_range(nblocks_total, world, r) for r in range(world)]
-    cap = max(hi - lo for lo, hi in sizes) * 8
-    buf = torch.zeros(cap, dtype=torch.uint8, device=local.device)
-    buf[:local.numel()] = local
-    parts = [torch.empty_like(buf) for _ in range(world)] if rank == dst else None
-    dist.gather(buf, parts, dst=dst)
+    lo, hi = sizes[rank]
+    if local.numel() != 8 * (hi - lo):
+        raise ValueError(f"rank {rank}: shard has {local.numel()} bytes, expected {8 * (hi - lo)}")
+    cap = max(h - l for l, h in sizes) * 8
+    ragged = any(h - l != cap // 8 for l, h in sizes)
+    send = local
+    if ragged:
+        send = torch.zeros(cap, dtype=torch.uint8, device=local.device)
+        send[:local.numel()] = local
     if rank != dst:
+        dist.gather(send, None, dst=dst)
         return None
-    return torch.cat([p[:(hi - lo) * 8] for p, (lo, hi) in zip(parts, sizes)])
+    out = torch.empty(world * cap, dtype=torch.uint8, device=local.device)
+    dist.gather(send, [out[r * cap:(r + 1) * cap] for r in range(world)], dst=dst)
+    if ragged:
+        for r, (l, h) in enumerate(sizes):   # destinations never pass their sources
+            if 8 * l != r * cap:
+                out[8 * l:8 * h] = out[r * cap:r * cap + 8 * (h - l)].clone()
+        out = out[:8 * nblocks_total]
+    return out

@@ -75,12 +75,3 @@ def random_blocks(rng: np.random.Generator, nblocks: int) -> np.ndarray:
 
 def random_key(rng: np.random.Generator) -> bytes:
     return bytes(rng.integers(0, 256, size=8, dtype=np.uint8).tolist())
-
-
-def shard_range(nblocks: int, world: int, rank: int) -> tuple[int, int]:
-    """Contiguous block range [lo, hi) owned by ``rank`` of ``world`` (ECB shards by range)."""
-    if world <= 0 or not 0 <= rank < world:
-        raise ValueError("bad world/rank")
-    lo = (nblocks * rank) // world
-    hi = (nblocks * (rank + 1)) // world
-    return lo, hi

@@ -100,3 +100,62 @@ def test_argument_validation_without_launch(tdes):
     assert lib.tdes_strerror(-3) == b"input and output partially overlap"
     ki = tdes.kernel_info()
     assert ki.blocks_per_thread == 32 and ki.sbox_lop3_total == sum(ki.sbox_lop3[g] for g in range(8))
+
+
+def test_nblocks_overflow_is_rejected_before_the_buffer_check(tdes):
+    """nblocks * 8 would wrap: rejected as INVALID_ARG before any overlap arithmetic."""
+    lib = tdes._lib
+    s = tdes.key_schedule(*synthetic.KEYS_3KEY)
+    huge = (1 << 64) // 8 + 1            # nblocks * 8 wraps to 8
+    assert lib.tdes_ecb_encrypt(ctypes.byref(s), 0x1000, 0x1000 + 8 * 2, huge, None) == -1
+    assert lib.tdes_ecb_crypt_mode(ctypes.byref(s), 0, 0x1000, 0x2000, (1 << 62), 1, None) == -1
+
+
+_ERR_SCRIPT = r"""
+import ctypes, sys
+sys.path.insert(0, {root!r})
+import paper_2007_10752_b200 as t
+lib = t._lib
+which = sys.argv[1]
+if which == "lop3":
+    ops = ctypes.c_uint64()
+    rc = lib.tdes_lop3_peak(0x10000, 1, 32, 1, ctypes.byref(ops), None)
+elif which == "fill":
+    rc = lib.tdes_fill_splitmix64(0x10000, 8, 0, 1, None)
+elif which == "paper":
+    rc = lib.tdes_paper_ecb(0x10000, 0x20000, 0x30000, 4, 0, 0x40000, 3 * 16 * 48, None)
+else:
+    s = t.key_schedule("0123456789ABCDEF", "23456789ABCDEF01", "456789ABCDEF0123")
+    rc = lib.tdes_ecb_encrypt(ctypes.byref(s), 0x10000, 0x20000, 4, None)
+print(rc, lib.tdes_last_cuda_error())
+"""
+
+
+@pytest.mark.parametrize("which", ["lop3", "fill", "paper", "encrypt"])
+def test_last_cuda_error_is_shared_by_every_entry_point(which):
+    """A TDES_ERR_CUDA from a tdes_bench.h / tdes_paper.h call sets the same
+    per-thread cudaError tdes_last_cuda_error() reports (include/tdes.h).  Without
+    a GPU every launch fails, so each entry point is driven to TDES_ERR_CUDA in a
+    fresh process (nothing set the error before)."""
+    import subprocess
+    import sys
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("needs a host without a usable GPU (launches must fail)")
+    out = subprocess.run([sys.executable, "-c", _ERR_SCRIPT.format(root=ROOT), which],
+                         capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stderr
+    rc, err = map(int, out.stdout.split())
+    assert rc == -4
+    assert err != 0          # a real cudaError_t (no device / insufficient driver), not a stale 0
+
+
+def test_debug_library_builds_and_exports(tdes):
+    """The TDES_DEBUG variant (device-pointer checks) is built by build() and exports the same ABI."""
+    lib_path = os.path.join(ROOT, "paper_2007_10752_b200", "libtdes_b200_debug.so")
+    if not os.path.exists(lib_path):
+        import __graft_entry__
+        __graft_entry__.build_library(debug=True)
+    lib = ctypes.CDLL(lib_path)
+    for n in tdes.EXPORTS:
+        assert hasattr(lib, n), n

@@ -360,3 +360,54 @@ def test_weak_keys_vs_oracle_and_involution(tdes, weak):
     c = tdes.ecb_encrypt(to_dev(p), s)
     assert np.array_equal(c.cpu().numpy(), oracle.tdes_ecb(weak, weak, weak, p))
     assert np.array_equal(tdes.ecb_encrypt(c, s).cpu().numpy(), p)
+
+
+_DEBUG_SCRIPT = r"""
+import ctypes, os, sys
+sys.path.insert(0, {root!r})
+import numpy as np, torch
+import paper_2007_10752_b200 as t
+import oracle, synthetic
+assert t.LIB_PATH.endswith("libtdes_b200_debug.so"), t.LIB_PATH
+torch.cuda.set_device(0)
+s = t.key_schedule(*synthetic.KEYS_3KEY)
+n = 4096
+p = synthetic.plaintext_bytes(0, n)
+host = torch.from_numpy(p.copy())
+pinned = host.pin_memory()
+dev = host.cuda()
+out = torch.empty_like(dev)
+lib = t._lib
+res = {{}}
+res["host_in"] = lib.tdes_ecb_encrypt(ctypes.byref(s), host.data_ptr(), out.data_ptr(), n, None)
+res["pinned_in"] = lib.tdes_ecb_encrypt(ctypes.byref(s), pinned.data_ptr(), out.data_ptr(), n, None)
+res["host_out"] = lib.tdes_ecb_encrypt(ctypes.byref(s), dev.data_ptr(), host.data_ptr(), n, None)
+res["split_host_in"] = lib.tdes_ecb_crypt_mode(ctypes.byref(s), 0, host.data_ptr(), out.data_ptr(), n, 2, None)
+res["device"] = lib.tdes_ecb_encrypt(ctypes.byref(s), dev.data_ptr(), out.data_ptr(), n, None)
+torch.cuda.synchronize()
+res["exact"] = bool(np.array_equal(out.cpu().numpy(), oracle.tdes_ecb(*synthetic.KEYS_3KEY, p)))
+print(res)
+"""
+
+
+def test_debug_build_rejects_host_pointers():
+    """libtdes_b200_debug.so (TDES_DEBUG) checks in/out with cudaPointerGetAttributes
+    and returns TDES_ERR_INVALID_ARG for host memory (include/tdes.h); device
+    buffers still run bit-exact."""
+    import ast
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    lib = os.path.join(root, "paper_2007_10752_b200", "libtdes_b200_debug.so")
+    if not os.path.exists(lib):
+        import __graft_entry__
+        __graft_entry__.build_library(debug=True)
+    env = dict(os.environ, TDES_LIB_PATH=lib)
+    out = subprocess.run([sys.executable, "-c", _DEBUG_SCRIPT.format(root=root)], env=env,
+                         capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr
+    res = ast.literal_eval(out.stdout.strip().splitlines()[-1])
+    assert res["host_in"] == -1 and res["pinned_in"] == -1 and res["host_out"] == -1
+    assert res["split_host_in"] == -1
+    assert res["device"] == 0 and res["exact"] is True

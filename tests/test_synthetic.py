@@ -30,19 +30,3 @@ def test_known_blocks():
     assert b == "F2497B8D145F1C0D" "D8C3B6368090297A"
     assert synthetic.plaintext_bytes(131071, 1).tobytes().hex().upper() == "C525B446280B2094"
 
-
-@pytest.mark.parametrize("n,g", [(1 << 20, 1), (1 << 20, 2), (1 << 20, 8), (1000, 3), (5, 8), (0, 4)])
-def test_shard_ranges_partition(n, g):
-    ranges = [synthetic.shard_range(n, g, r) for r in range(g)]
-    assert ranges[0][0] == 0 and ranges[-1][1] == n
-    for (a, b), (c, d) in zip(ranges, ranges[1:]):
-        assert b == c and a <= b
-    sizes = [b - a for a, b in ranges]
-    assert max(sizes) - min(sizes) <= 1
-
-
-def test_shard_range_rejects_bad_args():
-    with pytest.raises(ValueError):
-        synthetic.shard_range(10, 0, 0)
-    with pytest.raises(ValueError):
-        synthetic.shard_range(10, 2, 2)
