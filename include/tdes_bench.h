@@ -50,6 +50,9 @@ int tdes_lop3_peak(uint32_t *dev_sink, int grid, int cta, int iters, uint64_t *o
  *           kernel for small launches, the throughput kernel otherwise)
  *   mode 1  throughput kernel (32 blocks per thread, one warp per 1024-block tile)
  *   mode 2  S-box-split latency kernel (8 warps per tile, one S-box per warp)
+ *   mode 3  throughput kernel with device-side key expansion: the launch carries
+ *           only the 48 packed 48-bit subkeys (384 B); every CTA expands them into
+ *           the folded key operands in shared memory at start (NEXT-4)
  * Same arguments and errors as tdes_ecb_encrypt; decrypt 0/1. */
 int tdes_ecb_crypt_mode(const tdes_schedule *s, int decrypt, const void *in, void *out,
                         size_t nblocks, int mode, tdes_stream_t stream);

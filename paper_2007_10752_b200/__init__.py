@@ -98,7 +98,7 @@ EXPORTS = ("tdes_key_schedule", "tdes_ecb_encrypt", "tdes_ecb_decrypt", "des_key
            "tdes_count_mismatch", "tdes_lop3_peak", "tdes_device_geometry", "tdes_paper_ecb",
            "tdes_ecb_crypt_mode", "tdes_fold_operands")
 
-MODE_AUTO, MODE_THROUGHPUT, MODE_SPLIT = 0, 1, 2
+MODE_AUTO, MODE_THROUGHPUT, MODE_SPLIT, MODE_DEVKEYS = 0, 1, 2, 3
 
 
 def _check(rc: int, what: str):
@@ -196,7 +196,7 @@ def des_ecb_decrypt(x, sched: DesSchedule, out=None, stream=None):
 
 
 def ecb_crypt_mode(x: torch.Tensor, sched: TdesSchedule, mode: int, decrypt=False, out=None, stream=None):
-    """3DES ECB with an explicit kernel choice (MODE_AUTO / MODE_THROUGHPUT / MODE_SPLIT)."""
+    """3DES ECB with an explicit kernel choice (MODE_AUTO / MODE_THROUGHPUT / MODE_SPLIT / MODE_DEVKEYS)."""
     out = _prep(x, out)
     with torch.cuda.device(x.device):
         _check(_lib.tdes_ecb_crypt_mode(ctypes.byref(sched), int(bool(decrypt)), x.data_ptr(), out.data_ptr(),

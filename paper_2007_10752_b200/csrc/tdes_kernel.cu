@@ -24,6 +24,7 @@
 #include <string.h>
 
 #include <atomic>
+#include <type_traits>
 
 #include "../../include/tdes.h"
 #include "../../include/tdes_bench.h"
@@ -117,6 +118,95 @@ template <int NROUNDS>
 struct RoundKeys {
   uint64_t k[NROUNDS];  // bit 47 - b = subkey bit b (E position b), consumption order
 };
+
+// Mask folding, symbolically.  The planes' pending masks M are
+// tracked through the fused rounds exactly as the kernel applies them (fix-ups,
+// rounds, swaps): round r is round_A for even r, round_B for odd r, and a free
+// E-position of round r reads its plane as is, which is correct because the
+// previous round's unfused output (or a fix-up) set that plane's mask to the key
+// bit of exactly that position.  Every M is 0 or one key bit key(r, pos), and
+// which one depends only on the generator's plan, not on the key -- so every
+// operand word is key(a) ^ key(b) for a static pair of key-bit references
+// (index r * 48 + pos, kNoRef = none).  OpRefs holds those pairs; it is a
+// compile-time constant used by the host (build_masks) and, on the device, by
+// the throughput kernel's prologue, which expands the 384-byte packed subkeys
+// into its operand tables (NEXT-4, the paper's key-expansion step).
+constexpr uint16_t kNoRef = 0xFFFF;
+
+template <int NSTAGES>
+struct OpRefs {
+  static constexpr int NR = 16 * NSTAGES;
+  uint16_t sk[NR][tdes_gen::kKeyStride][2];   // s = v | 1, k = v
+  uint16_t d[NR][tdes_gen::kDeltaStride][2];  // folded-output masks
+  uint16_t fix[3][tdes_gen::kDeltaStride][2]; // fix_s = v | 1, fix_k = v
+  uint16_t fin[64];                           // fin_s = v | 1, fin_k = v (one reference)
+};
+
+template <int NSTAGES>
+constexpr OpRefs<NSTAGES> build_refs() {
+  using namespace tdes_gen;
+  constexpr int NR = 16 * NSTAGES;
+  OpRefs<NSTAGES> o{};
+  for (int r = 0; r < NR; ++r) {
+    for (int q = 0; q < kKeyStride; ++q) o.sk[r][q][0] = o.sk[r][q][1] = kNoRef;
+    for (int u = 0; u < kDeltaStride; ++u) o.d[r][u][0] = o.d[r][u][1] = kNoRef;
+  }
+  for (int b = 0; b < 3; ++b)
+    for (int t = 0; t < kDeltaStride; ++t) o.fix[b][t][0] = o.fix[b][t][1] = kNoRef;
+  uint16_t M[64] = {};
+  for (int j = 0; j < 64; ++j) M[j] = kNoRef;
+  auto key = [](int r, int pos) { return (uint16_t)(r * 48 + pos); };
+  auto boundary = [](int r) { return NSTAGES == 3 && (r == 16 || r == 32); };
+  auto fixup = [&](int b, int r) {  // prime round_A's free positions for round r
+    for (int t = 0; t < kFoldFree; ++t) {
+      const int pos = kFoldFreePos[0][t], j = kFoldSrc[0][pos];
+      o.fix[b][t][0] = M[j];
+      o.fix[b][t][1] = key(r, pos);
+      M[j] = key(r, pos);
+    }
+  };
+  fixup(0, 0);
+  for (int r = 0; r < NR; ++r) {
+    const int x = r & 1;
+    if (boundary(r)) {
+      for (int t = 0; t < 32; ++t) {
+        const uint16_t tmp = M[kHalfA[t]];
+        M[kHalfA[t]] = M[kHalfB[t]];
+        M[kHalfB[t]] = tmp;
+      }
+      fixup(r >> 4, r);
+    }
+    for (int q = 0; q < kKeySlots; ++q) {
+      const int pos = kFoldKeyPos[x][q];
+      o.sk[r][q][0] = M[kFoldSrc[x][pos]];
+      o.sk[r][q][1] = key(r, pos);
+    }
+    for (int u = 0; u < kFoldFree; ++u) {
+      const int j = kFoldUDst[x][u];
+      if (r + 1 < NR && !boundary(r + 1)) {
+        o.d[r][u][0] = M[j];
+        o.d[r][u][1] = key(r + 1, kFoldUNext[x][u]);
+        M[j] = key(r + 1, kFoldUNext[x][u]);
+      }  // else the mask stays: d = 0
+    }
+  }
+  for (int j = 0; j < 64; ++j) o.fin[j] = M[j];
+  return o;
+}
+
+constexpr OpRefs<3> kRefs3 = build_refs<3>();
+constexpr OpRefs<1> kRefs1 = build_refs<1>();
+template <int NSTAGES>
+constexpr const OpRefs<NSTAGES>& refs_host() {
+  if constexpr (NSTAGES == 3) return kRefs3; else return kRefs1;
+}
+// Device copies (read once per CTA by the prologue; 10 KB for 3DES).
+__device__ const OpRefs<3> kDevRefs3 = build_refs<3>();
+__device__ const OpRefs<1> kDevRefs1 = build_refs<1>();
+template <int NSTAGES>
+__device__ __forceinline__ const OpRefs<NSTAGES>& refs_dev() {
+  if constexpr (NSTAGES == 3) return kDevRefs3; else return kDevRefs1;
+}
 
 // Key-XOR form per variant (tdes_gen::kxor).  With k read from the launch
 // parameters, rebuilding k from s (MULHI) was 1.9x faster for single DES (ptxas
@@ -315,10 +405,11 @@ __device__ __forceinline__ void store_group(uint2* out, size_t base, size_t nblo
 // TMA staging (kTma): `staged` = this tile sits in `buf` (wait on `bar` with
 // `phase`); `prefetch` claims the warp's next tile and starts its copy into `buf`
 // once the current one has been read out of it.
-template <int NSTAGES, bool VEC4, class Prefetch>
+// KV = ParamKeys (host-folded operands in the launch parameters) or DevKeys
+// (operands expanded on the device into shared memory); see below.
+template <int NSTAGES, bool VEC4, class KV, class Prefetch>
 __device__ __forceinline__ void crypt_tile(const uint2* in, uint2* out, size_t base, size_t nblocks,
-                                           unsigned lane, const RoundMasks<16 * NSTAGES>& mk,
-                                           const uint4* ksm, uint32_t c, uint4* buf, uint64_t* bar,
+                                           unsigned lane, const KV& kv, uint32_t c, uint4* buf, uint64_t* bar,
                                            bool staged, uint32_t phase, Prefetch&& prefetch) {
   using V = typename PlaneOf<kWords>::type;
   V P[64];
@@ -354,29 +445,16 @@ __device__ __forceinline__ void crypt_tile(const uint2* in, uint2* out, size_t b
   // updated last, so at each stage boundary the halves swap
   // register roles and the same A-then-B body continues.
   constexpr int kUnroll = NSTAGES == 3 ? kRoundUnroll3 : 1;
-  constexpr int kKv = tdes_gen::kKeyStride / 4;              // k vectors per round
-  constexpr int kKq = kKv + tdes_gen::kDeltaStride / 4;      // k + d vectors per round in shared memory
-  tdes_gen::fold_fixup_A<kUseMulhi<NSTAGES>>(P, mk.fix_s[0], mk.fix_k[0], c);
+  kv.fixup(P, 0, c);
 #pragma unroll kUnroll
   for (int r = 0; r < 16 * NSTAGES; r += 2) {
     if (NSTAGES == 3 && (r == 16 || r == 32)) {
       tdes_gen::swap_halves(P);
-      tdes_gen::fold_fixup_A<kUseMulhi<NSTAGES>>(P, mk.fix_s[r >> 4], mk.fix_k[r >> 4], c);
+      kv.fixup(P, r >> 4, c);
     }
-    if (kKeySmem == 0 || kUseMulhi<NSTAGES>) {
-      tdes_gen::round_A<kUseMulhi<NSTAGES>>(P, mk.s[r], mk.k[r], mk.d[r], c);
-      tdes_gen::round_B<kUseMulhi<NSTAGES>>(P, mk.s[r + 1], mk.k[r + 1], mk.d[r + 1], c);
-    } else {  // k and d from the shared-memory table: [round][k | d] as uint4
-      const uint4* t0 = ksm + kKq * r;
-      const uint4* t1 = ksm + kKq * (r + 1);
-      // s as uint2 pairs: every uniform load is 64-bit, also for an odd slot count
-      const uint2* s0 = reinterpret_cast<const uint2*>(mk.s[r]);
-      const uint2* s1 = reinterpret_cast<const uint2*>(mk.s[r + 1]);
-      tdes_gen::round_A<false>(P, s0, t0, t0 + kKv, c);
-      tdes_gen::round_B<false>(P, s1, t1, t1 + kKv, c);
-    }
+    kv.two_rounds(P, r, c);
   }
-  tdes_gen::fold_unmask<kUseMulhi<NSTAGES>>(P, mk.fin_s, mk.fin_k, c);
+  kv.unmask(P, c);
   V Q[64];
   tdes_gen::output_planes(P, Q);
   // ---- S7: back to blocks, store ----
@@ -392,30 +470,152 @@ __device__ __forceinline__ void crypt_tile(const uint2* in, uint2* out, size_t b
   }
 }
 
+// ---- key operand sources of the throughput kernel ----
+// ParamKeys: the host-folded operands (RoundMasks, build_masks) are the launch
+// parameters; s is read as a uniform operand (LDCU) straight from them, k and d
+// from a shared-memory copy the CTA makes at start (one broadcast LDS.128 per
+// four values).  18 KB of parameters for 3DES.
+template <int NSTAGES>
+struct ParamKeys {
+  const RoundMasks<16 * NSTAGES>& mk;
+  const uint4* ksm;  // per round: kKv k vectors, then kDv d vectors
+  static constexpr int kKv = tdes_gen::kKeyStride / 4, kDv = tdes_gen::kDeltaStride / 4;
+  template <class V>
+  __device__ __forceinline__ void fixup(V (&P)[64], int b, uint32_t c) const {
+    tdes_gen::fold_fixup_A<kUseMulhi<NSTAGES>>(P, mk.fix_s[b], mk.fix_k[b], c);
+  }
+  template <class V>
+  __device__ __forceinline__ void two_rounds(V (&P)[64], int r, uint32_t c) const {
+    if (kKeySmem == 0 || kUseMulhi<NSTAGES>) {
+      tdes_gen::round_A<kUseMulhi<NSTAGES>>(P, mk.s[r], mk.k[r], mk.d[r], c);
+      tdes_gen::round_B<kUseMulhi<NSTAGES>>(P, mk.s[r + 1], mk.k[r + 1], mk.d[r + 1], c);
+    } else {  // k and d from the shared-memory table: [round][k | d] as uint4
+      const uint4* t0 = ksm + (kKv + kDv) * r;
+      const uint4* t1 = ksm + (kKv + kDv) * (r + 1);
+      // s as uint2 pairs: every uniform load is 64-bit, also for an odd slot count
+      const uint2* s0 = reinterpret_cast<const uint2*>(mk.s[r]);
+      const uint2* s1 = reinterpret_cast<const uint2*>(mk.s[r + 1]);
+      tdes_gen::round_A<false>(P, s0, t0, t0 + kKv, c);
+      tdes_gen::round_B<false>(P, s1, t1, t1 + kKv, c);
+    }
+  }
+  template <class V>
+  __device__ __forceinline__ void unmask(V (&P)[64], uint32_t c) const {
+    tdes_gen::fold_unmask<kUseMulhi<NSTAGES>>(P, mk.fin_s, mk.fin_k, c);
+  }
+};
+
+// DevKeys (NEXT-4): the launch carries only the 48 (16) packed subkeys in
+// consumption order (RoundKeys, 384 B); each CTA expands them at start into every
+// operand the rounds use -- s, k, d, fix-ups, final unmask -- as key(a) ^ key(b)
+// over the compile-time reference pairs OpRefs (expand_keys below), all in shared
+// memory.  The round reads s and k with broadcast LDS.128 into vector registers
+// (IMAD x * s + k with every operand a vector register).
+template <int NSTAGES>
+struct DevKeys {
+  static constexpr int kKv = tdes_gen::kKeyStride / 4, kDv = tdes_gen::kDeltaStride / 4;
+  static constexpr int kSt = 2 * kKv + kDv;  // uint4 per round: s | k | d
+  static constexpr int kTabVecs = kSt * 16 * NSTAGES;
+  static constexpr int kFixFinWords = 2 * 3 * tdes_gen::kDeltaStride + 2 * 64;
+  const uint4* tab;
+  const uint32_t* ff;  // fix_s[3][kDeltaStride] fix_k[3][kDeltaStride] fin_s[64] fin_k[64]
+  template <class V>
+  __device__ __forceinline__ void fixup(V (&P)[64], int b, uint32_t c) const {
+    tdes_gen::fold_fixup_A<false>(P, ff + tdes_gen::kDeltaStride * b, ff + tdes_gen::kDeltaStride * (3 + b), c);
+  }
+  template <class V>
+  __device__ __forceinline__ void two_rounds(V (&P)[64], int r, uint32_t c) const {
+    const uint4* t0 = tab + kSt * r;
+    const uint4* t1 = tab + kSt * (r + 1);
+    tdes_gen::round_A<false>(P, t0, t0 + kKv, t0 + 2 * kKv, c);
+    tdes_gen::round_B<false>(P, t1, t1 + kKv, t1 + 2 * kKv, c);
+  }
+  template <class V>
+  __device__ __forceinline__ void unmask(V (&P)[64], uint32_t c) const {
+    tdes_gen::fold_unmask<false>(P, ff + 6 * tdes_gen::kDeltaStride, ff + 6 * tdes_gen::kDeltaStride + 64, c);
+  }
+};
+
 // NSTAGES = 3: fused 3DES (48 rounds); NSTAGES = 1: single DES (16 rounds).
 // Work distribution: CTA c owns the contiguous tile range
 // [ntiles*c/grid, ntiles*(c+1)/grid); its warps claim tiles one at a time
 // from a shared-memory counter.  Warps of one SM progress at very different
 // rates under the hardware's warp arbitration, so a static per-warp split
 // leaves the SM waiting on its slowest warp (measured: 1.6-2x slower).
-template <int NSTAGES, bool VEC4>
+// Launch parameters of the key material: RoundMasks (host-folded, 18 KB for
+// 3DES) or RoundKeys (packed subkeys, 384 B; DEVKEYS).
+template <int NSTAGES, bool DEVKEYS>
+using KeyParam = std::conditional_t<DEVKEYS, RoundKeys<16 * NSTAGES>, RoundMasks<16 * NSTAGES>>;
+
+template <int NSTAGES, bool DEVKEYS>
+constexpr int kKeySmemVecs =
+    DEVKEYS ? DevKeys<NSTAGES>::kTabVecs + DevKeys<NSTAGES>::kFixFinWords / 4
+            : (kKeySmem == 0 || kUseMulhi<NSTAGES> ? 1 : (ParamKeys<NSTAGES>::kKv + ParamKeys<NSTAGES>::kDv) * 16 * NSTAGES);
+
+// DevKeys prologue: every operand word = key(a) ^ key(b) over OpRefs, the key
+// bits taken from the packed subkeys (bit 47 - pos of round r = E-position pos).
+template <int NSTAGES>
+__device__ __forceinline__ void expand_keys(const RoundKeys<16 * NSTAGES>& kp, uint4* smem) {
+  using DK = DevKeys<NSTAGES>;
+  using namespace tdes_gen;
+  constexpr int NR = 16 * NSTAGES;
+  const OpRefs<NSTAGES>& o = refs_dev<NSTAGES>();
+  auto bit = [&](uint16_t ref) -> uint32_t {
+    return ref == kNoRef ? 0u : 0u - (uint32_t)((kp.k[ref / 48] >> (47 - ref % 48)) & 1u);
+  };
+  uint32_t* t32 = reinterpret_cast<uint32_t*>(smem);
+  for (int i = threadIdx.x; i < NR * kKeyStride; i += blockDim.x) {
+    const int r = i / kKeyStride, q = i % kKeyStride;
+    const uint32_t v = bit(o.sk[r][q][0]) ^ bit(o.sk[r][q][1]);
+    t32[4 * (r * DK::kSt) + q] = v | 1u;        // s
+    t32[4 * (r * DK::kSt + DK::kKv) + q] = v;   // k
+  }
+  for (int i = threadIdx.x; i < NR * kDeltaStride; i += blockDim.x) {
+    const int r = i / kDeltaStride, u = i % kDeltaStride;
+    t32[4 * (r * DK::kSt + 2 * DK::kKv) + u] = bit(o.d[r][u][0]) ^ bit(o.d[r][u][1]);
+  }
+  uint32_t* ff = t32 + 4 * DK::kTabVecs;
+  for (int i = threadIdx.x; i < 3 * kDeltaStride; i += blockDim.x) {
+    const int b = i / kDeltaStride, t = i % kDeltaStride;
+    const uint32_t v = bit(o.fix[b][t][0]) ^ bit(o.fix[b][t][1]);
+    ff[i] = v | 1u;
+    ff[3 * kDeltaStride + i] = v;
+  }
+  for (int j = threadIdx.x; j < 64; j += blockDim.x) {
+    const uint32_t v = bit(o.fin[j]);
+    ff[6 * kDeltaStride + j] = v | 1u;
+    ff[6 * kDeltaStride + 64 + j] = v;
+  }
+}
+
+// NSTAGES = 3: fused 3DES (48 rounds); NSTAGES = 1: single DES (16 rounds).
+// DEVKEYS: key operands expanded on the device from the packed subkeys (DevKeys)
+// instead of host-folded launch parameters (ParamKeys).
+// Work distribution: CTA c owns the contiguous tile range
+// [ntiles*c/grid, ntiles*(c+1)/grid); its warps claim tiles one at a time
+// from a shared-memory counter.  Warps of one SM progress at very different
+// rates under the hardware's warp arbitration, so a static per-warp split
+// leaves the SM waiting on its slowest warp (measured: 1.6-2x slower).
+template <int NSTAGES, bool VEC4, bool DEVKEYS>
 __global__ void __launch_bounds__(kThreads, kMinCtasPerSm)
 tdes_ecb_kernel(const uint2* in, uint2* out, size_t nblocks,
-                const __grid_constant__ RoundMasks<16 * NSTAGES> mk, uint32_t c) {
+                const __grid_constant__ KeyParam<NSTAGES, DEVKEYS> kp, uint32_t c) {
   __shared__ unsigned int next_tile;
-  // shared-memory key table: per round the kKeySlots k operands then the unfused-output masks d
-  constexpr int kKv = tdes_gen::kKeyStride / 4, kDv = tdes_gen::kDeltaStride / 4;
-  constexpr int kKeyVecs = (kKv + kDv) * 16 * NSTAGES;
-  __shared__ uint4 ksm[kKeySmem == 0 || kUseMulhi<NSTAGES> ? 1 : kKeyVecs];  // k, 9 KiB for 3DES
+  // shared-memory key table: ParamKeys per round the kKeySlots k operands then the
+  // unfused-output masks d (9 KiB for 3DES); DevKeys every operand (18 KiB)
+  __shared__ uint4 ksm[kKeySmemVecs<NSTAGES, DEVKEYS>];
   const unsigned lane = threadIdx.x & 31u;
   const size_t ntiles = (nblocks + kTileBlocks - 1) / kTileBlocks;
   const size_t lo = ntiles * blockIdx.x / gridDim.x;
   const size_t hi = ntiles * (blockIdx.x + 1) / gridDim.x;
   if (threadIdx.x == 0) next_tile = 0;
-  if (kKeySmem != 0 && !kUseMulhi<NSTAGES>) {
-    const uint4* k4 = reinterpret_cast<const uint4*>(&mk.k[0][0]);
-    const uint4* d4 = reinterpret_cast<const uint4*>(&mk.d[0][0]);
-    for (int i = threadIdx.x; i < kKeyVecs; i += blockDim.x) {
+  if constexpr (DEVKEYS) {
+    expand_keys<NSTAGES>(kp, ksm);
+  } else if (kKeySmem != 0 && !kUseMulhi<NSTAGES>) {
+    constexpr int kKv = ParamKeys<NSTAGES>::kKv, kDv = ParamKeys<NSTAGES>::kDv;
+    const uint4* k4 = reinterpret_cast<const uint4*>(&kp.k[0][0]);
+    const uint4* d4 = reinterpret_cast<const uint4*>(&kp.d[0][0]);
+    for (int i = threadIdx.x; i < kKeySmemVecs<NSTAGES, false>; i += blockDim.x) {
       const int r = i / (kKv + kDv), q = i % (kKv + kDv);
       ksm[i] = q < kKv ? k4[r * kKv + q] : d4[r * kDv + q - kKv];
     }
@@ -434,6 +634,13 @@ tdes_ecb_kernel(const uint2* in, uint2* out, size_t nblocks,
   };
   // a tile is staged by TMA when it is full (16-byte aligned, VEC4 path)
   auto stageable = [&](size_t t) { return kTma && VEC4 && t < hi && (t + 1) * kTileBlocks <= nblocks; };
+  using KV = std::conditional_t<DEVKEYS, DevKeys<NSTAGES>, ParamKeys<NSTAGES>>;
+  const KV kv = [&]() {
+    if constexpr (DEVKEYS)
+      return KV{ksm, reinterpret_cast<const uint32_t*>(ksm + DevKeys<NSTAGES>::kTabVecs)};
+    else
+      return KV{kp, ksm};
+  }();
   size_t tile = claim();
   bool staged = stageable(tile);
   if (staged && lane == 0) tma_load(buf, in + tile * kTileBlocks, kTileBytes, &tma_bar[warp]);
@@ -446,8 +653,8 @@ tdes_ecb_kernel(const uint2* in, uint2* out, size_t nblocks,
       next_staged = stageable(next);
       if (lane == 0 && next_staged) tma_load(buf, in + next * kTileBlocks, kTileBytes, &tma_bar[warp]);
     };
-    crypt_tile<NSTAGES, VEC4>(in, out, tile * kTileBlocks, nblocks, lane, mk, ksm, c, buf, &tma_bar[warp],
-                              staged, phase, prefetch);
+    crypt_tile<NSTAGES, VEC4>(in, out, tile * kTileBlocks, nblocks, lane, kv, c, buf, &tma_bar[warp], staged,
+                              phase, prefetch);
     if (staged) phase ^= 1u;
     if (kTma) {
       tile = next;
@@ -642,25 +849,25 @@ tdes_split_kernel(const uint2* in, uint2* out, size_t nblocks,
 
 constexpr int kMaxDevices = 64;
 std::atomic<int> g_sms[kMaxDevices];
-std::atomic<int> g_occ[kMaxDevices][2][2];  // [dev][stages==3][vec4]
+std::atomic<int> g_occ[kMaxDevices][2][2][2];  // [dev][stages==3][vec4][devkeys]
 
 template <bool VEC4>
 constexpr size_t kDynSmem = kTma && VEC4 ? (size_t)kWarps * kTileBytes : 0;
 
 // Also raises the kernel's dynamic shared-memory limit (TMA buffers) once per device.
-template <int NSTAGES, bool VEC4>
+template <int NSTAGES, bool VEC4, bool DEVKEYS>
 int occupancy(int dev) {
-  int v = g_occ[dev][NSTAGES == 3][VEC4].load(std::memory_order_relaxed);
+  int v = g_occ[dev][NSTAGES == 3][VEC4][DEVKEYS].load(std::memory_order_relaxed);
   if (v > 0) return v;
   int occ = 0;
   if (kDynSmem<VEC4> > 0)
-    cudaFuncSetAttribute(tdes_ecb_kernel<NSTAGES, VEC4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(tdes_ecb_kernel<NSTAGES, VEC4, DEVKEYS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kDynSmem<VEC4>);
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tdes_ecb_kernel<NSTAGES, VEC4>, kThreads,
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tdes_ecb_kernel<NSTAGES, VEC4, DEVKEYS>, kThreads,
                                                     kDynSmem<VEC4>) != cudaSuccess ||
       occ <= 0)
     occ = kMinCtasPerSm;
-  g_occ[dev][NSTAGES == 3][VEC4].store(occ, std::memory_order_relaxed);
+  g_occ[dev][NSTAGES == 3][VEC4][DEVKEYS].store(occ, std::memory_order_relaxed);
   return occ;
 }
 
@@ -691,57 +898,39 @@ int check_buffers(const void* in, const void* out, size_t nblocks) {
 // 1024-block tiles, the throughput kernel above (measured crossover).
 constexpr size_t kSplitMaxTiles = 296;
 constexpr size_t kSplitSpecMaxTiles = 16;  // the S-box-specialised split kernel (tdes_split_kernel<., true>)
+// Auto mode: the throughput kernel with device-expanded key operands (mode 3)
+// up to this many tiles, the host-folded one (mode 1) above.  Its 384-byte
+// launch parameters start ~2 us sooner than the 18 KB block, but its s operands
+// come from shared memory instead of the uniform path, which costs 6.5% on long
+// launches (B200, tools/exp/size_timing.py: 2^19 blocks 24.7 -> 23.3 us back to
+// back, 2^20 equal, 2^21 59.8 -> 61.6 us, 1 GiB 2792 -> 2983 us).
+constexpr size_t kDevKeysMaxTiles = 768;
 
-// Host side of mask folding: simulate the planes' pending masks M through the
-// fused rounds exactly as the kernel applies them (fix-ups, rounds, swaps) and
-// emit the operands.  Round r is round_A for even r, round_B for odd r; a free
-// E-position of round r reads its plane as is, which is correct because the
-// previous round's unfused output (or a fix-up) set that plane's mask to the key
-// bit of exactly that position.
+// Host: the operand words for key masks `masks` (consumption order, 0 / ~0).
 template <int NSTAGES>
 void build_masks(const uint32_t (*masks)[48], RoundMasks<16 * NSTAGES>& mk) {
   using namespace tdes_gen;
   constexpr int NR = 16 * NSTAGES;
+  const OpRefs<NSTAGES>& o = refs_host<NSTAGES>();
+  auto bit = [&](uint16_t ref) -> uint32_t { return ref == kNoRef ? 0u : (masks[ref / 48][ref % 48] ? ~0u : 0u); };
   memset(&mk, 0, sizeof mk);
-  uint32_t M[64] = {0};
-  auto key = [&](int r, int pos) { return masks[r][pos] ? 0xFFFFFFFFu : 0u; };
-  auto boundary = [&](int r) { return NSTAGES == 3 && (r == 16 || r == 32); };
-  auto fixup = [&](int b, int r) {  // prime round_A's free positions for round r
-    for (int t = 0; t < kFoldFree; ++t) {
-      const int pos = kFoldFreePos[0][t], j = kFoldSrc[0][pos];
-      const uint32_t v = M[j] ^ key(r, pos);
-      mk.fix_s[b][t] = v | 1u;
-      mk.fix_k[b][t] = v;
-      M[j] = key(r, pos);
-    }
-  };
-  fixup(0, 0);
   for (int r = 0; r < NR; ++r) {
-    const int x = r & 1;
-    if (boundary(r)) {
-      for (int t = 0; t < 32; ++t) {
-        const uint32_t tmp = M[kHalfA[t]];
-        M[kHalfA[t]] = M[kHalfB[t]];
-        M[kHalfB[t]] = tmp;
-      }
-      fixup(r >> 4, r);
-    }
     for (int q = 0; q < kKeySlots; ++q) {
-      const int pos = kFoldKeyPos[x][q];
-      const uint32_t v = M[kFoldSrc[x][pos]] ^ key(r, pos);
+      const uint32_t v = bit(o.sk[r][q][0]) ^ bit(o.sk[r][q][1]);
       mk.s[r][q] = v | 1u;  // s = k | 1
       mk.k[r][q] = v;
     }
-    for (int u = 0; u < kFoldFree; ++u) {
-      const int j = kFoldUDst[x][u];
-      const uint32_t want = r + 1 < NR && !boundary(r + 1) ? key(r + 1, kFoldUNext[x][u]) : M[j];
-      mk.d[r][u] = M[j] ^ want;
-      M[j] = want;
-    }
+    for (int u = 0; u < kFoldFree; ++u) mk.d[r][u] = bit(o.d[r][u][0]) ^ bit(o.d[r][u][1]);
   }
+  for (int b = 0; b < 3; ++b)
+    for (int t = 0; t < kFoldFree; ++t) {
+      const uint32_t v = bit(o.fix[b][t][0]) ^ bit(o.fix[b][t][1]);
+      mk.fix_s[b][t] = v | 1u;
+      mk.fix_k[b][t] = v;
+    }
   for (int j = 0; j < 64; ++j) {
-    mk.fin_s[j] = M[j] | 1u;
-    mk.fin_k[j] = M[j];
+    mk.fin_s[j] = bit(o.fin[j]) | 1u;
+    mk.fin_k[j] = bit(o.fin[j]);
   }
 }
 
@@ -767,7 +956,39 @@ const RoundMasks<16 * NSTAGES>& cached_masks(const uint32_t (*masks)[48]) {
   return e.mk;
 }
 
-// mode: 0 auto, 1 throughput kernel, 2 split (latency) kernel.
+// The consumption-order key masks packed one 48-bit word per round (bit 47 - b =
+// E-position b): the 384-byte launch parameter of the split kernel and of the
+// device-key throughput kernel.
+template <int NSTAGES>
+RoundKeys<16 * NSTAGES> pack_keys(const uint32_t (*masks)[48]) {
+  RoundKeys<16 * NSTAGES> ms;
+  for (int r = 0; r < 16 * NSTAGES; ++r) {
+    uint64_t w = 0;
+    for (int b = 0; b < 48; ++b) w = (w << 1) | (masks[r][b] ? 1u : 0u);
+    ms.k[r] = w;
+  }
+  return ms;
+}
+
+template <int NSTAGES, bool DEVKEYS>
+cudaError_t launch_throughput(const KeyParam<NSTAGES, DEVKEYS>& kp, const uint2* pin, uint2* pout, size_t nblocks,
+                              bool vec4, int dev, cudaStream_t stream) {
+  // one resident CTA per SM; with fewer tiles than SMs, one tile per CTA
+  const size_t ntiles = (nblocks + kTileBlocks - 1) / kTileBlocks;
+  const int occ = vec4 ? occupancy<NSTAGES, true, DEVKEYS>(dev) : occupancy<NSTAGES, false, DEVKEYS>(dev);
+  const size_t resident = (size_t)num_sms(dev) * (size_t)occ;
+  const unsigned grid = (unsigned)(ntiles < resident ? ntiles : resident);
+  if (vec4)
+    tdes_ecb_kernel<NSTAGES, true, DEVKEYS><<<grid, kThreads, kDynSmem<true>, stream>>>(pin, pout, nblocks, kp,
+                                                                                         kMulhiC);
+  else
+    tdes_ecb_kernel<NSTAGES, false, DEVKEYS><<<grid, kThreads, kDynSmem<false>, stream>>>(pin, pout, nblocks, kp,
+                                                                                           kMulhiC);
+  return cudaGetLastError();
+}
+
+// mode: 0 auto, 1 throughput kernel (host-folded key operands), 2 split
+// (latency) kernel, 3 throughput kernel with device-expanded key operands.
 template <int NSTAGES>
 int launch(const uint32_t (*masks)[48], const void* in, void* out, size_t nblocks,
            cudaStream_t stream, int mode = 0) {
@@ -784,12 +1005,7 @@ int launch(const uint32_t (*masks)[48], const void* in, void* out, size_t nblock
   if (mode == 2 || (mode == 0 && ngroups <= kSplitMaxTiles)) {
     const size_t cap = (size_t)num_sms(dev) * 8u;  // up to 8 teams per SM
     const unsigned sgrid = (unsigned)(ngroups < cap ? ngroups : cap);
-    RoundKeys<16 * NSTAGES> ms;
-    for (int r = 0; r < 16 * NSTAGES; ++r) {
-      uint64_t w = 0;
-      for (int b = 0; b < 48; ++b) w = (w << 1) | (masks[r][b] ? 1u : 0u);
-      ms.k[r] = w;
-    }
+    const RoundKeys<16 * NSTAGES> ms = pack_keys<NSTAGES>(masks);
     if (ngroups <= kSplitSpecMaxTiles)
       tdes_split_kernel<NSTAGES, true><<<sgrid, kSplitThreads, 0, stream>>>(
           static_cast<const uint2*>(in), static_cast<uint2*>(out), nblocks, ms, kMulhiC);
@@ -799,20 +1015,12 @@ int launch(const uint32_t (*masks)[48], const void* in, void* out, size_t nblock
     e = cudaGetLastError();
     return e == cudaSuccess ? TDES_OK : cuda_fail(e);
   }
-  const RoundMasks<16 * NSTAGES>& mk = cached_masks<NSTAGES>(masks);
-  // one resident CTA per SM; with fewer tiles than SMs, one tile per CTA
-  const size_t ntiles = (nblocks + kTileBlocks - 1) / kTileBlocks;
-  const int occ = vec4 ? occupancy<NSTAGES, true>(dev) : occupancy<NSTAGES, false>(dev);
-  const size_t resident = (size_t)num_sms(dev) * (size_t)occ;
-  const unsigned grid = (unsigned)(ntiles < resident ? ntiles : resident);
   const uint2* pin = static_cast<const uint2*>(in);
   uint2* pout = static_cast<uint2*>(out);
-  if (vec4)
-    tdes_ecb_kernel<NSTAGES, true><<<grid, kThreads, kDynSmem<true>, stream>>>(pin, pout, nblocks, mk, kMulhiC);
+  if (mode == 3 || (mode == 0 && ngroups <= kDevKeysMaxTiles))
+    e = launch_throughput<NSTAGES, true>(pack_keys<NSTAGES>(masks), pin, pout, nblocks, vec4, dev, stream);
   else
-    tdes_ecb_kernel<NSTAGES, false><<<grid, kThreads, kDynSmem<false>, stream>>>(pin, pout, nblocks, mk,
-                                                                                 kMulhiC);
-  e = cudaGetLastError();
+    e = launch_throughput<NSTAGES, false>(cached_masks<NSTAGES>(masks), pin, pout, nblocks, vec4, dev, stream);
   if (e != cudaSuccess) return cuda_fail(e);
   return TDES_OK;
 }
@@ -833,7 +1041,7 @@ extern "C" int tdes_ecb_decrypt(const tdes_schedule* s, const void* in, void* ou
 
 extern "C" int tdes_ecb_crypt_mode(const tdes_schedule* s, int decrypt, const void* in, void* out,
                                    size_t nblocks, int mode, tdes_stream_t stream) {
-  if (!s || (decrypt != 0 && decrypt != 1) || mode < 0 || mode > 2) return TDES_ERR_INVALID_ARG;
+  if (!s || (decrypt != 0 && decrypt != 1) || mode < 0 || mode > 3) return TDES_ERR_INVALID_ARG;
   return launch<3>(s->mask[decrypt], in, out, nblocks, reinterpret_cast<cudaStream_t>(stream), mode);
 }
 
@@ -953,6 +1161,6 @@ extern "C" int tdes_device_geometry(int* sms, int* ctas_per_sm) {
   if (e != cudaSuccess) return cuda_fail(e);
   if (dev < 0 || dev >= kMaxDevices) return TDES_ERR_INVALID_ARG;
   *sms = num_sms(dev);
-  *ctas_per_sm = occupancy<3, true>(dev);
+  *ctas_per_sm = occupancy<3, true, false>(dev);
   return TDES_OK;
 }

@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--log2n", type=int, default=27)
     ap.add_argument("--op", default="enc", choices=["enc", "dec", "des"])
     ap.add_argument("--launches", type=int, default=4)
+    ap.add_argument("--mode", type=int, default=None, help="force a 3DES kernel (tdes_ecb_crypt_mode)")
     a = ap.parse_args()
     n = 1 << a.log2n
     x = torch.empty(8 * n, dtype=torch.uint8, device="cuda")
@@ -28,7 +29,9 @@ def main():
     s = tdes.key_schedule(*synthetic.KEYS_3KEY)
     ds = tdes.des_key_schedule(synthetic.KEYS_1KEY[0])
     for _ in range(a.launches):
-        if a.op == "enc":
+        if a.mode is not None and a.op in ("enc", "dec"):
+            tdes.ecb_crypt_mode(x, s, a.mode, decrypt=a.op == "dec", out=y)
+        elif a.op == "enc":
             tdes.ecb_encrypt(x, s, out=y)
         elif a.op == "dec":
             tdes.ecb_decrypt(x, s, out=y)
