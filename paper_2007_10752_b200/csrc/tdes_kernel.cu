@@ -480,18 +480,9 @@ struct ParamKeys {
   const RoundMasks<16 * NSTAGES>& mk;
   const uint4* ksm;  // per round: kKv k vectors, then kDv d vectors
   static constexpr int kKv = tdes_gen::kKeyStride / 4, kDv = tdes_gen::kDeltaStride / 4;
-  template <int TS = 1, int TW = 0, class V>
+  template <class V>
   __device__ __forceinline__ void fixup(V (&P)[64], int b, uint32_t c) const {
-    tdes_gen::fold_fixup_A<kUseMulhi<NSTAGES>, TS, TW>(P, mk.fix_s[b], mk.fix_k[b], c);
-  }
-  // One round r (H = 0: round_A, 1: round_B), the S-boxes of team warp TW only.
-  template <int H, int TS, int TW, class V>
-  __device__ __forceinline__ void round(V (&P)[64], int r, uint32_t c) const {
-    static_assert(kKeySmem != 0 && !kUseMulhi<NSTAGES>, "team mode reads k from shared memory");
-    const uint4* t = ksm + (kKv + kDv) * r;
-    const uint2* sp = reinterpret_cast<const uint2*>(mk.s[r]);
-    if constexpr (H == 0) tdes_gen::round_A<false, TS, TW>(P, sp, t, t + kKv, c);
-    else tdes_gen::round_B<false, TS, TW>(P, sp, t, t + kKv, c);
+    tdes_gen::fold_fixup_A<kUseMulhi<NSTAGES>>(P, mk.fix_s[b], mk.fix_k[b], c);
   }
   template <class V>
   __device__ __forceinline__ void two_rounds(V (&P)[64], int r, uint32_t c) const {
@@ -528,16 +519,9 @@ struct DevKeys {
   static constexpr int kFixFinWords = 2 * 3 * tdes_gen::kDeltaStride + 2 * 64;
   const uint4* tab;
   const uint32_t* ff;  // fix_s[3][kDeltaStride] fix_k[3][kDeltaStride] fin_s[64] fin_k[64]
-  template <int TS = 1, int TW = 0, class V>
+  template <class V>
   __device__ __forceinline__ void fixup(V (&P)[64], int b, uint32_t c) const {
-    tdes_gen::fold_fixup_A<false, TS, TW>(P, ff + tdes_gen::kDeltaStride * b, ff + tdes_gen::kDeltaStride * (3 + b),
-                                          c);
-  }
-  template <int H, int TS, int TW, class V>
-  __device__ __forceinline__ void round(V (&P)[64], int r, uint32_t c) const {
-    const uint4* t = tab + kSt * r;
-    if constexpr (H == 0) tdes_gen::round_A<false, TS, TW>(P, t, t + kKv, t + 2 * kKv, c);
-    else tdes_gen::round_B<false, TS, TW>(P, t, t + kKv, t + 2 * kKv, c);
+    tdes_gen::fold_fixup_A<false>(P, ff + tdes_gen::kDeltaStride * b, ff + tdes_gen::kDeltaStride * (3 + b), c);
   }
   template <class V>
   __device__ __forceinline__ void two_rounds(V (&P)[64], int r, uint32_t c) const {
@@ -677,151 +661,6 @@ tdes_ecb_kernel(const uint2* in, uint2* out, size_t nblocks,
       staged = next_staged;
     } else {
       tile = claim();
-    }
-  }
-}
-
-
-// ------------------------------------------------------- team (mid-size) mode -----
-// With a few tiles per SMSP the throughput kernel runs each tile on one warp whose
-// in-order issue is dependency bound (ncu at 2^19 blocks: ALU pipe 47% busy, stalls
-// `wait` and `short_scoreboard`), so a launch lasts about one tile's 48 serial rounds.
-// Here TS warps share a tile: warp TW evaluates S-boxes 8/TS*TW .. 8/TS*(TW+1)-1 --
-// the paper's idea of spreading one block's round over several threads,
-// at S-box-group granularity.  Every warp holds the whole state in registers; a
-// plane position is owned by the warp whose S-box writes it, and after each round
-// the owners publish through shared memory (st[plane][lane]) exactly the updated
-// planes the other warps read next (tdes_gen::team_publish / team_receive; 10-11
-// per warp per round for TS = 2), one named barrier per round and team.  Key
-// operands, mask folding, fix-ups and the stage-boundary swaps are the throughput
-// kernel's (the generated round functions restricted to the warp's S-boxes).
-__device__ __forceinline__ void team_bar(int team, int nthreads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(team + 1), "r"(nthreads) : "memory");
-}
-
-template <int NSTAGES, int TS, int TW, bool VEC4, class KV>
-__device__ __forceinline__ void team_tile(const uint2* in, uint2* out, size_t base, size_t nblocks, unsigned lane,
-                                          const KV& kv, uint32_t c, uint32_t* st, int team) {
-  uint32_t P[64];
-  {
-    uint32_t X[32], Y[32];
-    load_group<VEC4>(in, base, nblocks, lane, X, Y);
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      P[j] = X[j];
-      P[32 + j] = Y[j];
-    }
-  }
-  kv.template fixup<TS, TW>(P, 0, c);
-#pragma unroll 1
-  for (int r = 0; r < 16 * NSTAGES; r += 2) {
-    if (NSTAGES == 3 && (r == 16 || r == 32)) {
-      tdes_gen::swap_halves(P);
-      kv.template fixup<TS, TW>(P, r >> 4, c);
-    }
-    kv.template round<0, TS, TW>(P, r, c);
-    tdes_gen::team_publish<TS, TW, 0>(P, st, lane);
-    team_bar(team, 32 * TS);
-    tdes_gen::team_receive<TS, TW, 0>(P, st, lane);
-    kv.template round<1, TS, TW>(P, r + 1, c);
-    tdes_gen::team_publish<TS, TW, 1>(P, st, lane);
-    team_bar(team, 32 * TS);
-    tdes_gen::team_receive<TS, TW, 1>(P, st, lane);
-  }
-  team_bar(team, 32 * TS);  // every warp is past its last receive before st is rewritten
-  tdes_gen::team_publish_owned<TS, TW>(P, st, lane);
-  team_bar(team, 32 * TS);
-  tdes_gen::team_receive_rest<TS, TW>(P, st, lane);
-  kv.unmask(P, c);
-  uint32_t Q[64];
-  tdes_gen::output_planes(P, Q);
-  uint32_t X[32], Y[32];
-#pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    X[j] = Q[j];
-    Y[j] = Q[32 + j];
-  }
-  transpose32(X);
-  transpose32(Y);
-  // each warp stores its share of the tile (same lane layout as store_group)
-  const bool full = base + kGroupBlocks <= nblocks;
-  if (VEC4) {
-    uint4* out4 = reinterpret_cast<uint4*>(out + base);
-#pragma unroll
-    for (int i = 16 * TW / TS; i < 16 * (TW + 1) / TS; ++i) {
-      const size_t b = base + 64 * i + 2 * lane;
-      const uint4 v = make_uint4(X[2 * i], Y[2 * i], X[2 * i + 1], Y[2 * i + 1]);
-      if (full || b + 1 < nblocks) {
-        __stcs(out4 + 32 * i + lane, v);
-      } else if (b < nblocks) {
-        __stcs(out + b, make_uint2(v.x, v.y));
-      }
-    }
-  } else {
-#pragma unroll
-    for (int i = 32 * TW / TS; i < 32 * (TW + 1) / TS; ++i) {
-      const size_t b = base + 32 * i + lane;
-      if (full || b < nblocks) __stcs(out + b, make_uint2(X[i], Y[i]));
-    }
-  }
-}
-
-template <int TS>
-constexpr size_t kTeamSmem = (size_t)(kWarps / TS) * 64 * 32 * sizeof(uint32_t);
-
-template <int NSTAGES, int TS, bool VEC4, bool DEVKEYS>
-__global__ void __launch_bounds__(kThreads, 1)
-tdes_team_kernel(const uint2* in, uint2* out, size_t nblocks, const __grid_constant__ KeyParam<NSTAGES, DEVKEYS> kp,
-                 uint32_t c) {
-  static_assert(kWarps % TS == 0 && kWarps / TS <= 15, "named barriers 1..15");
-  constexpr int kTeams = kWarps / TS;
-  __shared__ unsigned int next_tile;
-  __shared__ unsigned int team_claim[kTeams];
-  __shared__ uint4 ksm[kKeySmemVecs<NSTAGES, DEVKEYS>];
-  extern __shared__ uint32_t xst[];  // [kTeams][64 planes][32 lanes]
-  const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-  const int team = (int)(warp / TS), tw = (int)(warp % TS);
-  const size_t ntiles = (nblocks + kGroupBlocks - 1) / kGroupBlocks;
-  const size_t lo = ntiles * blockIdx.x / gridDim.x;
-  const size_t hi = ntiles * (blockIdx.x + 1) / gridDim.x;
-  if (threadIdx.x == 0) next_tile = 0;
-  if constexpr (DEVKEYS) {
-    expand_keys<NSTAGES>(kp, ksm);
-  } else {
-    constexpr int kKv = ParamKeys<NSTAGES>::kKv, kDv = ParamKeys<NSTAGES>::kDv;
-    const uint4* k4 = reinterpret_cast<const uint4*>(&kp.k[0][0]);
-    const uint4* d4 = reinterpret_cast<const uint4*>(&kp.d[0][0]);
-    for (int i = threadIdx.x; i < kKeySmemVecs<NSTAGES, false>; i += blockDim.x) {
-      const int r = i / (kKv + kDv), q = i % (kKv + kDv);
-      ksm[i] = q < kKv ? k4[r * kKv + q] : d4[r * kDv + q - kKv];
-    }
-  }
-  __syncthreads();
-  using KV = std::conditional_t<DEVKEYS, DevKeys<NSTAGES>, ParamKeys<NSTAGES>>;
-  const KV kv = [&]() {
-    if constexpr (DEVKEYS)
-      return KV{ksm, reinterpret_cast<const uint32_t*>(ksm + DevKeys<NSTAGES>::kTabVecs)};
-    else
-      return KV{kp, ksm};
-  }();
-  uint32_t* st = xst + (size_t)team * 64 * 32;
-  for (;;) {
-    if (tw == 0 && lane == 0) team_claim[team] = atomicAdd(&next_tile, 1u);
-    team_bar(team, 32 * TS);
-    const size_t tile = lo + team_claim[team];
-    if (tile >= hi) break;
-    const size_t base = tile * kGroupBlocks;
-    // a compile-time S-box group per warp (warp-uniform branch)
-    if constexpr (TS == 2) {
-      if (tw == 0) team_tile<NSTAGES, 2, 0, VEC4>(in, out, base, nblocks, lane, kv, c, st, team);
-      else team_tile<NSTAGES, 2, 1, VEC4>(in, out, base, nblocks, lane, kv, c, st, team);
-    } else {
-      switch (tw) {
-        case 0: team_tile<NSTAGES, 4, 0, VEC4>(in, out, base, nblocks, lane, kv, c, st, team); break;
-        case 1: team_tile<NSTAGES, 4, 1, VEC4>(in, out, base, nblocks, lane, kv, c, st, team); break;
-        case 2: team_tile<NSTAGES, 4, 2, VEC4>(in, out, base, nblocks, lane, kv, c, st, team); break;
-        default: team_tile<NSTAGES, 4, 3, VEC4>(in, out, base, nblocks, lane, kv, c, st, team); break;
-      }
     }
   }
 }
@@ -1148,34 +987,8 @@ cudaError_t launch_throughput(const KeyParam<NSTAGES, DEVKEYS>& kp, const uint2*
   return cudaGetLastError();
 }
 
-template <int NSTAGES, int TS, bool DEVKEYS>
-cudaError_t launch_team(const KeyParam<NSTAGES, DEVKEYS>& kp, const uint2* pin, uint2* pout, size_t nblocks,
-                        bool vec4, int dev, cudaStream_t stream) {
-  static std::atomic<int> attr_set[kMaxDevices][2];
-  if (!attr_set[dev][vec4].exchange(1)) {
-    if (vec4)
-      cudaFuncSetAttribute(tdes_team_kernel<NSTAGES, TS, true, DEVKEYS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)kTeamSmem<TS>);
-    else
-      cudaFuncSetAttribute(tdes_team_kernel<NSTAGES, TS, false, DEVKEYS>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTeamSmem<TS>);
-  }
-  const size_t ntiles = (nblocks + kGroupBlocks - 1) / kGroupBlocks;
-  const size_t sms = (size_t)num_sms(dev);
-  const unsigned grid = (unsigned)(ntiles < sms ? ntiles : sms);
-  if (vec4)
-    tdes_team_kernel<NSTAGES, TS, true, DEVKEYS><<<grid, kThreads, kTeamSmem<TS>, stream>>>(pin, pout, nblocks, kp,
-                                                                                             kMulhiC);
-  else
-    tdes_team_kernel<NSTAGES, TS, false, DEVKEYS><<<grid, kThreads, kTeamSmem<TS>, stream>>>(pin, pout, nblocks,
-                                                                                              kp, kMulhiC);
-  return cudaGetLastError();
-}
-
 // mode: 0 auto, 1 throughput kernel (host-folded key operands), 2 split
-// (latency) kernel, 3 throughput kernel with device-expanded key operands,
-// 4 / 5 team kernel with 2 / 4 warps per tile (host-folded key operands),
-// 6 / 7 the same with device-expanded key operands.
+// (latency) kernel, 3 throughput kernel with device-expanded key operands.
 template <int NSTAGES>
 int launch(const uint32_t (*masks)[48], const void* in, void* out, size_t nblocks,
            cudaStream_t stream, int mode = 0) {
@@ -1204,13 +1017,6 @@ int launch(const uint32_t (*masks)[48], const void* in, void* out, size_t nblock
   }
   const uint2* pin = static_cast<const uint2*>(in);
   uint2* pout = static_cast<uint2*>(out);
-  if (mode >= 4) {
-    if (mode == 4) e = launch_team<NSTAGES, 2, false>(cached_masks<NSTAGES>(masks), pin, pout, nblocks, vec4, dev, stream);
-    else if (mode == 5) e = launch_team<NSTAGES, 4, false>(cached_masks<NSTAGES>(masks), pin, pout, nblocks, vec4, dev, stream);
-    else if (mode == 6) e = launch_team<NSTAGES, 2, true>(pack_keys<NSTAGES>(masks), pin, pout, nblocks, vec4, dev, stream);
-    else e = launch_team<NSTAGES, 4, true>(pack_keys<NSTAGES>(masks), pin, pout, nblocks, vec4, dev, stream);
-    return e == cudaSuccess ? TDES_OK : cuda_fail(e);
-  }
   if (mode == 3 || (mode == 0 && ngroups <= kDevKeysMaxTiles))
     e = launch_throughput<NSTAGES, true>(pack_keys<NSTAGES>(masks), pin, pout, nblocks, vec4, dev, stream);
   else
@@ -1235,7 +1041,7 @@ extern "C" int tdes_ecb_decrypt(const tdes_schedule* s, const void* in, void* ou
 
 extern "C" int tdes_ecb_crypt_mode(const tdes_schedule* s, int decrypt, const void* in, void* out,
                                    size_t nblocks, int mode, tdes_stream_t stream) {
-  if (!s || (decrypt != 0 && decrypt != 1) || mode < 0 || mode > 7) return TDES_ERR_INVALID_ARG;
+  if (!s || (decrypt != 0 && decrypt != 1) || mode < 0 || mode > 3) return TDES_ERR_INVALID_ARG;
   return launch<3>(s->mask[decrypt], in, out, nblocks, reinterpret_cast<cudaStream_t>(stream), mode);
 }
 

@@ -399,9 +399,7 @@ def emit_round(half, plan):
              "// as is (mask folding: its pending mask already equals the key bit); D = the masks",
              "// the unfused outputs fold into their planes.",
              "// S, K, D point to uint32_t or uint4 arrays (kat reads word i of either).",
-             "// TS, TW: team mode (csrc/tdes_kernel.cu tdes_team_kernel) -- only the S-boxes of",
-             "// warp TW of a TS-warp team (S-boxes 8/TS*TW .. 8/TS*(TW+1)-1); TS = 1: all.",
-             "template <bool MULHI, int TS = 1, int TW = 0, class V, class SP, class KP, class DP>",
+             "template <bool MULHI, class V, class SP, class KP, class DP>",
              f"__device__ __forceinline__ void round_{half}(V (&P)[64], const SP* __restrict__ S,",
              "                                        const KP* __restrict__ K, const DP* __restrict__ D, uint32_t c) {"]
     for g in SBOX_ORDER:
@@ -415,9 +413,8 @@ def emit_round(half, plan):
                 xs.append(f"P[{src[T.E[pos] - 1]}]")
         ds = [f"P[{out_plane(half, g, o)}]" for o in range(4)]
         ms = [f"kat<{uidx[(g, o)]}>(D)" if (g, o) in uidx else "0u" for o in range(4)]
-        lines.append(f"  if constexpr (TS == 1 || {g} * TS / 8 == TW)")
-        lines.append(f"    sbox{g + 1}({', '.join(xs)},")
-        lines.append(f"          {', '.join(ds)}, {', '.join(ms)});")
+        lines.append(f"  sbox{g + 1}({', '.join(xs)},")
+        lines.append(f"        {', '.join(ds)}, {', '.join(ms)});")
     lines.append("}")
     return "\n".join(lines)
 
@@ -446,17 +443,12 @@ def emit_fold(plan):
          "",
          "// Set the pending masks of round_A's free positions (before round 0 and after",
          "// the stage-boundary swaps): plane ^= s/k pair t (kxor).",
-         "// Team mode (TS > 1): only the planes warp TW holds (owns or reads).",
-         "template <bool MULHI, int TS = 1, int TW = 0, class V>",
+         "template <bool MULHI, class V>",
          "__device__ __forceinline__ void fold_fixup_A(V (&P)[64], const uint32_t* __restrict__ S,",
          "                                             const uint32_t* __restrict__ K, uint32_t c) {"]
     for t, i in enumerate(plan["A"]["free"]):
         j = plan["A"]["src"][i]
-        pos = B_IDX.index(j)   # round A reads half B
-        held = " || ".join(f"(TS == {ts} && TW == {tw})" for ts in TEAM_SIZES for tw in range(ts)
-                           if pos in team_sets(ts, tw)[0] | team_sets(ts, tw)[1])
-        h.append(f"  if constexpr (TS == 1{' || ' + held if held else ''})")
-        h.append(f"    P[{j}] = kxor<MULHI>(P[{j}], S[{t}], MULHI ? 0u : K[{t}], c);")
+        h.append(f"  P[{j}] = kxor<MULHI>(P[{j}], S[{t}], MULHI ? 0u : K[{t}], c);")
     h += ["}", "",
           "// Remove every plane's pending mask (after the last round).",
           "template <bool MULHI, class V>",
@@ -465,88 +457,6 @@ def emit_fold(plan):
           "#pragma unroll",
           "  for (int j = 0; j < 64; ++j) P[j] = kxor<MULHI>(P[j], S[j], MULHI ? 0u : K[j], c);",
           "}", ""]
-    return h
-
-
-# ---------------------------------------------------------------- team mode --
-# tdes_team_kernel (csrc/tdes_kernel.cu): TS warps share one 1024-block tile; warp TW
-# evaluates S-boxes 8/TS*TW .. 8/TS*(TW+1)-1.  A plane position i (0..31 of a half)
-# is OWNED by the warp whose S-box output lands there (P is a permutation), and
-# only the owner ever updates it; a warp READS the positions its S-boxes' E windows
-# take.  After each round the owners publish the updated half's planes that other
-# warps read, and each warp receives the planes it reads but does not own -- so
-# owned and read planes are always current in a warp's registers, the rest are dead.
-TEAM_SIZES = (2, 4)
-
-
-def team_sets(ts, tw):
-    """(owned positions, read positions) of warp tw of a ts-warp team."""
-    per = 8 // ts
-    boxes = range(tw * per, (tw + 1) * per)
-    owned = {i for i in range(32) if P_SRC[i] // 4 in boxes}
-    read = {T.E[6 * g + k] - 1 for g in boxes for k in range(6)}
-    return owned, read
-
-
-def emit_team():
-    halves = (A_IDX, B_IDX)
-    h = ["// ---- team mode: plane exchange between the warps of a tile team ----",
-         "// st[plane * 32 + lane]: the team's shared exchange area (64 planes x 32 lanes).",
-         "// team_publish<TS, TW, H>: warp TW's owned planes of half H (0 = A, 1 = B) that",
-         "// another warp reads; team_receive<TS, TW, H>: the planes of half H warp TW reads",
-         "// but does not own.  team_publish_owned / team_receive_rest: every owned plane /",
-         "// every other plane (the final gather before the output transpose).",
-         "template <int TS, int TW, int H, class V>",
-         "__device__ __forceinline__ void team_publish(const V (&P)[64], uint32_t* st, unsigned lane) {"]
-
-    def chain(fn):
-        out, first = [], True
-        for ts in TEAM_SIZES:
-            for tw in range(ts):
-                for hh in (0, 1):
-                    planes = fn(ts, tw, hh)
-                    cond = f"TS == {ts} && TW == {tw} && H == {hh}"
-                    out.append(f"  {'if' if first else 'else if'} constexpr ({cond}) {{")
-                    first = False
-                    out += [f"    {x}" for x in planes]
-                    out.append("  }")
-        return out
-
-    def pub(ts, tw, hh):
-        own, _ = team_sets(ts, tw)
-        others = set().union(*(team_sets(ts, w)[1] for w in range(ts) if w != tw))
-        return [f"st[{halves[hh][i]} * 32 + lane] = P[{halves[hh][i]}];" for i in sorted(own & others)]
-
-    def recv(ts, tw, hh):
-        own, rd = team_sets(ts, tw)
-        return [f"P[{halves[hh][i]}] = st[{halves[hh][i]} * 32 + lane];" for i in sorted(rd - own)]
-    h += chain(pub)
-    h += ["}", "", "template <int TS, int TW, int H, class V>",
-          "__device__ __forceinline__ void team_receive(V (&P)[64], const uint32_t* st, unsigned lane) {"]
-    h += chain(recv)
-    h += ["}", ""]
-
-    def owned_planes(ts, tw):
-        own, _ = team_sets(ts, tw)
-        return sorted(halves[hh][i] for hh in (0, 1) for i in own)
-
-    def chain2(fn):
-        out, first = [], True
-        for ts in TEAM_SIZES:
-            for tw in range(ts):
-                out.append(f"  {'if' if first else 'else if'} constexpr (TS == {ts} && TW == {tw}) {{")
-                first = False
-                out += [f"    {x}" for x in fn(ts, tw)]
-                out.append("  }")
-        return out
-    h += ["template <int TS, int TW, class V>",
-          "__device__ __forceinline__ void team_publish_owned(const V (&P)[64], uint32_t* st, unsigned lane) {"]
-    h += chain2(lambda ts, tw: [f"st[{j} * 32 + lane] = P[{j}];" for j in owned_planes(ts, tw)])
-    h += ["}", "", "template <int TS, int TW, class V>",
-          "__device__ __forceinline__ void team_receive_rest(V (&P)[64], const uint32_t* st, unsigned lane) {"]
-    h += chain2(lambda ts, tw: [f"P[{j}] = st[{j} * 32 + lane];" for j in range(64)
-                                if j not in owned_planes(ts, tw)])
-    h += ["}", ""]
     return h
 
 
@@ -745,7 +655,6 @@ def emit_header(circs):
         h.append(f"  Q[{k}] = P[{OUT_SRC[k]}];")
     h.append("}")
     h.append("")
-    h += emit_team()
     h += emit_split_tables()
     h.append("}  // namespace tdes_gen")
     h.append("")
