@@ -171,6 +171,13 @@ class ClockSampler:
         if self.ok:
             self._stop.set()
             self.t.join()
+            self._sample()   # at least one sample at the end of the timed region
+
+    def _sample(self):
+        try:
+            self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+        except Exception:
+            pass
 
     def summary(self):
         if not self.ok or not self.samples:
@@ -336,6 +343,13 @@ class CudaOps:
     def sync(self):
         self.torch.cuda.synchronize(self.dev)
 
+    @staticmethod
+    def wait(ev):
+        """Wait for `ev` by polling with sleeps: the GIL stays free for the clock
+        sampler thread during the timed region."""
+        while not ev.query():
+            time.sleep(0.0005)
+
 
 def step_launches(ops, wl, sched, x, y, n):
     """One step: one fused launch (c2, c4) or encrypt + in-place decrypt (c5)."""
@@ -386,6 +400,7 @@ def rank_loop(ops, workload: str, rank: int, world: int, steps: int, warmup: int
                 ops.record(ends[k])
                 k += 1
         ops.record(t_end)
+        ops.wait(t_end)
         ops.sync()
     barrier()
     local_ms = ops.elapsed_ms(t_begin, t_end)

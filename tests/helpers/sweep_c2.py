@@ -23,18 +23,37 @@ import synthetic  # noqa: E402
 
 
 def dev_time(fn, reps=10):
+    """(queued, idle, back-to-back) ms per launch, medians of `reps`.
+
+    queued: the launch is submitted behind a ~0.3 ms device-side sleep, so the
+            events bracket the launch's device time alone (front end + kernel);
+    idle:   events around one launch on an idle GPU (adds host submission latency);
+    b2b:    20 launches back to back, per launch."""
     for _ in range(3):
         fn()
     torch.cuda.synchronize()
-    ts = []
+    q, i = [], []
     for _ in range(reps):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
         fn()
         b.record()
         b.synchronize()
-        ts.append(a.elapsed_time(b))
-    return sorted(ts)[len(ts) // 2]
+        i.append(a.elapsed_time(b))
+        torch.cuda._sleep(600_000)
+        a.record()
+        fn()
+        b.record()
+        b.synchronize()
+        q.append(a.elapsed_time(b))
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda._sleep(600_000)
+    a.record()
+    for _ in range(20):
+        fn()
+    b.record()
+    b.synchronize()
+    return sorted(q)[len(q) // 2], sorted(i)[len(i) // 2], a.elapsed_time(b) / 20
 
 
 def check(keys, x, y, decrypt, n):
@@ -73,11 +92,13 @@ def main():
     rate = None
     lines = ["# Config 2: size sweep, 3DES-EDE ECB on one B200 vs the oracle on host cores", "",
              f"GPU: {torch.cuda.get_device_name(0)}; host cores used by the oracle: {cores} (OpenMP over blocks).",
-             "Device time = one launch (median of 10, CUDA events, data resident in HBM).",
+             "Device time = one launch queued behind a device-side sleep (median of 10, CUDA events, data",
+             "resident in HBM): the launch's own device time, no host submission latency.  Beside it: the",
+             "same launch on an idle GPU (adds the host's submission latency) and 20 launches back to back.",
              "Oracle = `oracle/tdes_oracle.c` (char per bit, as in the paper), wall clock;",
              "`~` = extrapolated from a timed sample (the full size would exceed the per-point cap).", "",
-             "| blocks | bytes | op | keys | GPU ms | GPU GB/s | bit-exact (blocks checked) | oracle s | oracle GB/s | GPU/oracle |",
-             "|---|---|---|---|---|---|---|---|---|---|"]
+             "| blocks | bytes | op | keys | GPU ms | GPU GB/s | idle-launch GB/s | back-to-back GB/s | bit-exact (blocks checked) | oracle s | oracle GB/s | GPU/oracle |",
+             "|---|---|---|---|---|---|---|---|---|---|---|---|"]
     points = [(e, op, "3-key") for e in range(17, 28) for op in ("enc", "dec")]
     points += [(25, op, k) for k in ("1-key", "2-key") for op in ("enc", "dec")]
     keysets = {"3-key": synthetic.KEYS_3KEY, "2-key": synthetic.KEYS_2KEY, "1-key": synthetic.KEYS_1KEY}
@@ -88,13 +109,14 @@ def main():
         dec = op == "dec"
         fn = tdes.ecb_decrypt if dec else tdes.ecb_encrypt
         xs, ys = x[:8 * n], y[:8 * n]
-        ms = dev_time(lambda: fn(xs, s, out=ys))
+        ms, ms_idle, ms_b2b = dev_time(lambda: fn(xs, s, out=ys))
         ok, nchk = check(keys, xs, ys, dec, n)
         osec, full, r = oracle_time(keys, n, a.cap, rate)
         rate = rate or r
         gbs = n * 8 / ms / 1e6
         ogbs = n * 8 / osec / 1e9
         lines.append(f"| 2^{e} | {n * 8 / 2**20:g} MiB | {op} | {kname} | {ms:.4f} | {gbs:.1f} | "
+                     f"{n * 8 / ms_idle / 1e6:.1f} | {n * 8 / ms_b2b / 1e6:.1f} | "
                      f"{'yes' if ok else 'NO'} ({nchk}) | {'' if full else '~'}{osec:.2f} | {ogbs:.4f} | "
                      f"{gbs / ogbs:.0f}x |")
         print(lines[-1], flush=True)

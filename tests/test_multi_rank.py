@@ -176,6 +176,10 @@ class StubOps:
     def sync(self):
         pass
 
+    @staticmethod
+    def wait(ev):
+        pass
+
 
 def _bench_worker(rank, world, port, workload, per_gpu, q):
     import sys

@@ -70,8 +70,8 @@ def save(best):
         f.write("\n")
 
 
-def run_one(g, circ, secs, seed, slack):
-    p = subprocess.run([BIN, str(secs), str(seed), str(slack)], input=to_stdin(g, circ),
+def run_one(g, circ, secs, seed, slack, depth_mode=0):
+    p = subprocess.run([BIN, str(secs), str(seed), str(slack), "4", str(depth_mode)], input=to_stdin(g, circ),
                        capture_output=True, text=True)
     found = []
     for line in p.stdout.splitlines():
@@ -93,6 +93,8 @@ def main():
     ap.add_argument("--slack", type=int, default=6)
     ap.add_argument("--rounds", type=int, default=1, help="restart from the improved circuits this often")
     ap.add_argument("--seed", type=int, default=int(time.time()) & 0xFFFF)
+    ap.add_argument("--depth-mode", action="store_true",
+                    help="minimise (gates, depth): bring a reduced circuit's depth back down")
     a = ap.parse_args()
     build()
     boxes = [int(b) - 1 for b in a.boxes.split(",")]
@@ -101,12 +103,12 @@ def main():
     for rnd in range(a.rounds):
         start = current_best()
         for g, c in saved.items():
-            if len(c["gates"]) < len(start[g]["gates"]):
+            if (len(c["gates"]), depth(c)) < (len(start[g]["gates"]), depth(start[g])):
                 start[g] = c
         tasks = []
         for i in range(max(a.jobs, len(boxes))):
             g = boxes[i % len(boxes)]
-            tasks.append((g, start[g], a.seconds, seed, a.slack))
+            tasks.append((g, start[g], a.seconds, seed, a.slack, int(a.depth_mode)))
             seed += 1
         with ThreadPoolExecutor(a.jobs) as ex:
             for g, sd, found in ex.map(lambda t: run_one(*t), tasks):
@@ -114,7 +116,7 @@ def main():
                     key = (len(c["gates"]), depth(c))
                     old = saved.get(g)
                     if old is None or key < (len(old["gates"]), depth(old)):
-                        if len(c["gates"]) < len(start[g]["gates"]) or old is not None:
+                        if key < (len(start[g]["gates"]), depth(start[g])) or old is not None:
                             saved[g] = dict(c, sbox=g, seed=sd)
                             save(saved)
                             print(f"round {rnd}: S{g + 1} -> {len(c['gates'])} gates, depth {depth(c)} "

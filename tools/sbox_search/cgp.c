@@ -16,8 +16,12 @@
  * Input (stdin): one line  "<t0> <t1> <t2> <t3>"  (64-bit truth tables, hex),
  *   one line "<ngates>", ngates lines "<lut> <a> <b> <c>", then four output lines
  *   "p <sig> <neg>" or "f <u> <v> <h>".
- * Usage: cgp <seconds> <seed> <slack> [lambda]
+ * Usage: cgp <seconds> <seed> <slack> [lambda] [depth_mode]
  *   slack = extra (initially inactive) gate slots available to the search.
+ *   depth_mode = 1: minimise (gates, depth) lexicographically -- a child is accepted
+ *   only if it is no worse in either order, and every strictly better circuit is
+ *   printed (used to bring a reduced circuit's depth back down: a deeper S-box
+ *   lengthens the round's critical path).
  * Output (stdout): every strictly better circuit found, as one JSON line
  *   {"gates": [[lut, a, b, c], ...], "outputs": [...], "neg": [...], "fuse": [...]}
  * with inactive gates removed and signals renumbered.  Exact verification is
@@ -182,6 +186,7 @@ int main(int argc, char **argv) {
   uint64_t rs = strtoull(argv[2], 0, 10) * 0x9E3779B97F4A7C15ull + 1;
   const int slack = atoi(argv[3]);
   const int lambda = argc > 4 ? atoi(argv[4]) : 4;
+  const int depth_mode = argc > 5 ? atoi(argv[5]) : 0;
   for (int i = 0; i < 6; i++) {
     VARS[i] = 0;
     for (int v = 0; v < 64; v++) if ((v >> (5 - i)) & 1) VARS[i] |= 1ull << v;
@@ -233,7 +238,7 @@ int main(int argc, char **argv) {
     fprintf(stderr, "initial circuit is not exact\n");
     return 3;
   }
-  int pd = depth(&p, act), best = pc;
+  int pd = depth(&p, act), best = pc, bestd = pd;
   const int d0 = pd;
   fprintf(stderr, "start: %d gates, depth %d\n", pc, pd);
   const clock_t t0 = clock();
@@ -255,6 +260,20 @@ int main(int argc, char **argv) {
       }
     }
     if (!have) continue;
+    if (depth_mode) {
+      if (bc < pc || (bc == pc && bd <= pd)) {
+        p = bestc;
+        pc = bc;
+        pd = bd;
+        if (bc < best || (bc == best && bd < bestd)) {
+          best = bc;
+          bestd = bd;
+          fprintf(stderr, "gen %ld: %d gates, depth %d\n", gen, bc, bd);
+          print_json(&p);
+        }
+      }
+      continue;
+    }
     /* neutral drift: accept equal cost as long as the depth stays within 2 of the start */
     if (bc < pc || bd <= d0 + 2) {
       p = bestc;

@@ -30,6 +30,7 @@ KEYS = [
     "sm__inst_executed_pipe_adu.avg.pct_of_peak_sustained_active",
     "smsp__issue_active.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum",
     "sm__thread_inst_executed_pipe_alu_pred_on.sum",
+    "smsp__inst_executed_pipe_alu.sum", "smsp__inst_executed_pipe_fma.sum",
     "dram__bytes_read.sum", "dram__bytes_write.sum", "dram__throughput.avg.pct_of_peak_sustained_elapsed",
     "sm__throughput.avg.pct_of_peak_sustained_elapsed",
 ]
@@ -72,6 +73,8 @@ def main():
     ap.add_argument("--blocks", type=int, required=True, help="blocks processed by the profiled launch")
     ap.add_argument("--tag", required=True)
     ap.add_argument("--note", default="")
+    ap.add_argument("--aux", action="store_true",
+                    help="a side capture: write only the summary, not ncu_traffic.json / kernel_counters.json")
     a = ap.parse_args()
     m = raw_metrics(a.rep)
     lines = [f"# ncu summary {a.tag}", "", a.note, "",
@@ -109,10 +112,30 @@ def main():
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     with open(os.path.join(ROOT, "profiles", f"ncu_{a.tag}.md"), "w") as f:
         f.write("\n".join(lines) + "\n")
+    if a.aux:
+        print("\n".join(lines))
+        return
     with open(os.path.join(ROOT, "profiles", "ncu_traffic.json"), "w") as f:
         json.dump({"dram_bytes_per_block": per_block, "source": f"profiles/ncu_{a.tag}.md",
                    "blocks": a.blocks}, f, indent=1)
         f.write("\n")
+    alu = to_float(m.get("smsp__inst_executed_pipe_alu.sum", (None, ""))[0])
+    if alu:
+        fma = to_float(m.get("smsp__inst_executed_pipe_fma.sum", ("0", ""))[0]) or 0.0
+        allw = to_float(m.get("smsp__inst_executed.sum", ("0", ""))[0]) or 0.0
+        pct = to_float(m.get("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active", ("0", ""))[0])
+        with open(os.path.join(ROOT, "profiles", "kernel_counters.json"), "w") as f:
+            json.dump({"source": f"profiles/ncu_{a.tag}.md ({os.path.basename(a.rep)})", "blocks": a.blocks,
+                       "alu_warp_inst": alu, "fma_warp_inst": fma, "all_warp_inst": allw,
+                       "alu_thread_inst_per_block": alu * 32 / a.blocks,
+                       "fma_thread_inst_per_block": fma * 32 / a.blocks,
+                       "all_thread_inst_per_block": allw * 32 / a.blocks,
+                       "alu_pipe_pct": pct,
+                       "note": "alu_thread_inst_per_block counts every ALU-pipe instruction the kernel issues per "
+                               "block (S-box gates and Feistel XORs = 48 (T + 32) / 32 algorithmic, the "
+                               "load/store transposes ~20, loop and epilogue the rest); times blocks/s over "
+                               "(148 SMs x 64 lanes x clock) it is the ALU pipe's busy fraction"}, f, indent=1)
+            f.write("\n")
     print("\n".join(lines))
 
 
