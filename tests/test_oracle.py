@@ -285,3 +285,14 @@ def test_against_pyca_cryptography():
         p = synthetic.random_blocks(rng, 257)
         for dec in (False, True):
             assert oracle.tdes_ecb(k1, k2, k3, p, decrypt=dec).tobytes() == run(k1, k2, k3, p, dec)
+
+
+def test_feistel_f_worked_example(kat_rows):
+    """oracle_feistel_f against the printed round-1 value of the classic worked
+    example (tests/golden/des_kat.txt FEISTEL rows): f(R0, K1) = 234AA9BB, and
+    L0 xor f = R1 = EF4A6544 (§III.B: E, key XOR, S-boxes, P)."""
+    rows = [f for kind, f, cite in kat_rows if kind == "FEISTEL"]
+    assert rows
+    for r, k, f in rows:
+        assert oracle.feistel_f(int(r, 16), int(k, 16)) == int(f, 16)
+    assert 0xCC00CCFF ^ oracle.feistel_f(0xF0AAF0AA, 0x1B02EFFC7072) == 0xEF4A6544
