@@ -9,6 +9,7 @@ S-box table (gen_tdes.verify_circuit) before it is written to
 tools/circuits/lut3_cgp.json (per S-box the fewest gates, then the lowest depth).
 
   python tools/run_cgp.py --seconds 600 [--boxes 1,5,7] [--jobs 8] [--slack 6] [--rounds 3]
+                          [--mode drift|depth|budget] [--weight 16]
 """
 import argparse
 import json
@@ -70,8 +71,8 @@ def save(best):
         f.write("\n")
 
 
-def run_one(g, circ, secs, seed, slack, depth_mode=0):
-    p = subprocess.run([BIN, str(secs), str(seed), str(slack), "4", str(depth_mode)], input=to_stdin(g, circ),
+def run_one(g, circ, secs, seed, slack, mode=0, weight=16):
+    p = subprocess.run([BIN, str(secs), str(seed), str(slack), "4", str(mode), str(weight)], input=to_stdin(g, circ),
                        capture_output=True, text=True)
     found = []
     for line in p.stdout.splitlines():
@@ -93,8 +94,10 @@ def main():
     ap.add_argument("--slack", type=int, default=6)
     ap.add_argument("--rounds", type=int, default=1, help="restart from the improved circuits this often")
     ap.add_argument("--seed", type=int, default=int(time.time()) & 0xFFFF)
-    ap.add_argument("--depth-mode", action="store_true",
-                    help="minimise (gates, depth): bring a reduced circuit's depth back down")
+    ap.add_argument("--mode", choices=["drift", "depth", "budget"], default="drift",
+                    help="drift: exact circuits only, equal-cost moves accepted; depth: minimise (gates, depth); "
+                         "budget: may trade exactness for one gate less and drift back (cgp.c mode 2)")
+    ap.add_argument("--weight", type=int, default=16, help="budget mode: wrong bits per gate over budget")
     a = ap.parse_args()
     build()
     boxes = [int(b) - 1 for b in a.boxes.split(",")]
@@ -108,7 +111,8 @@ def main():
         tasks = []
         for i in range(max(a.jobs, len(boxes))):
             g = boxes[i % len(boxes)]
-            tasks.append((g, start[g], a.seconds, seed, a.slack, int(a.depth_mode)))
+            tasks.append((g, start[g], a.seconds, seed, a.slack, {"drift": 0, "depth": 1, "budget": 2}[a.mode],
+                          a.weight))
             seed += 1
         with ThreadPoolExecutor(a.jobs) as ex:
             for g, sd, found in ex.map(lambda t: run_one(*t), tasks):

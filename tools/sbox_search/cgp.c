@@ -18,6 +18,10 @@
  *   "p <sig> <neg>" or "f <u> <v> <h>".
  * Usage: cgp <seconds> <seed> <slack> [lambda] [depth_mode]
  *   slack = extra (initially inactive) gate slots available to the search.
+ *   depth_mode = 2: budget mode -- fitness = wrong output bits + W x (active gates
+ *   above the best count - 1), W = argv[6] (default 16); a child is accepted if its
+ *   fitness is no worse, so the search may give up exactness to drop a gate and
+ *   then drift back to an exact circuit one gate smaller (printed when found).
  *   depth_mode = 1: minimise (gates, depth) lexicographically -- a child is accepted
  *   only if it is no worse in either order, and every strictly better circuit is
  *   printed (used to bring a reduced circuit's depth back down: a deeper S-box
@@ -187,6 +191,7 @@ int main(int argc, char **argv) {
   const int slack = atoi(argv[3]);
   const int lambda = argc > 4 ? atoi(argv[4]) : 4;
   const int depth_mode = argc > 5 ? atoi(argv[5]) : 0;
+  const int weight = argc > 6 ? atoi(argv[6]) : 16;
   for (int i = 0; i < 6; i++) {
     VARS[i] = 0;
     for (int v = 0; v < 64; v++) if ((v >> (5 - i)) & 1) VARS[i] |= 1ull << v;
@@ -243,6 +248,34 @@ int main(int argc, char **argv) {
   fprintf(stderr, "start: %d gates, depth %d\n", pc, pd);
   const clock_t t0 = clock();
   long gen = 0;
+  if (depth_mode == 2) {
+    int budget = pc - 1;
+    int pf = weight;  /* parent fitness: exact, one gate over budget */
+    for (;;) {
+      if ((++gen & 0xFFFF) == 0 && (double)(clock() - t0) / CLOCKS_PER_SEC > secs) break;
+      for (int l = 0; l < lambda; l++) {
+        G c = p;
+        mutate(&c, &rs);
+        uint8_t ca[MAXN];
+        const int cc = active(&c, ca);
+        const int ce = errors(&c, ca);
+        const int cf = ce + weight * (cc > budget ? cc - budget : 0);
+        if (cf <= pf) {
+          p = c;
+          pf = cf;
+          if (ce == 0 && cc <= budget) {
+            fprintf(stderr, "gen %ld: %d gates, depth %d\n", gen, cc, depth(&c, ca));
+            print_json(&p);
+            budget = cc - 1;
+            pf = weight;
+          }
+          break;
+        }
+      }
+    }
+    fprintf(stderr, "done: %ld generations, budget %d\n", gen, budget);
+    return 0;
+  }
   for (;;) {
     if ((++gen & 0xFFFF) == 0 && (double)(clock() - t0) / CLOCKS_PER_SEC > secs) break;
     G bestc;
