@@ -169,10 +169,27 @@ def load_searched():
                 continue
             prefer = os.environ.get("TDES_GEN_PREFER", "")  # experiment: "S:file.json,..." wins ties
             preferred = f"{g + 1}:{os.path.basename(path)}" in prefer.split(",")
-            if g not in best or circuit_cost(circ) < circuit_cost(best[g]) or (
-                    preferred and circuit_cost(circ) == circuit_cost(best[g])):
-                best[g] = circ
+            if g not in best or preferred or circuit_rank(circ) < circuit_rank(best[g]):
+                if not (g in best and preferred and circuit_cost(circ) > circuit_cost(best[g])):
+                    best[g] = circ
     return best
+
+
+def circuit_depth(circ) -> int:
+    d = [0] * 6
+    for lut, a, b, c in circ["gates"]:
+        d.append(1 + max(d[a], d[b], d[c]))
+    return max(d[s] if f is None else max(d[f[0]], d[f[1]])
+               for s, f in zip(circ["outputs"], circ.get("fuse") or [None] * 4))
+
+
+def circuit_rank(circ):
+    """Choice among verified circuits of one S-box: fewest gates, then the most
+    outputs that can fold a key mask (each saves the round one key IMAD; measured
+    worth about half a gate), then the lowest depth."""
+    n = normalize_outputs(circ)
+    folds = sum(1 for o, f in enumerate(n.get("fuse") or [None] * 4) if f is None or o in fold_producers(n))
+    return (circuit_cost(circ), -folds, circuit_depth(circ))
 
 
 def normalize_outputs(circ):

@@ -34,13 +34,11 @@ def build():
 
 
 def depth(circ):
-    d = [0] * 6
-    for lut, a, b, c in circ["gates"]:
-        d.append(1 + max(d[a], d[b], d[c]))
-    m = 0
-    for s, f in zip(circ["outputs"], circ.get("fuse") or [None] * 4):
-        m = max(m, d[s] if f is None else max(d[f[0]], d[f[1]]))
-    return m
+    return gen_tdes.circuit_depth(circ)
+
+
+def rank(circ):
+    return gen_tdes.circuit_rank(circ)
 
 
 def to_stdin(g, circ):
@@ -94,9 +92,10 @@ def main():
     ap.add_argument("--slack", type=int, default=6)
     ap.add_argument("--rounds", type=int, default=1, help="restart from the improved circuits this often")
     ap.add_argument("--seed", type=int, default=int(time.time()) & 0xFFFF)
-    ap.add_argument("--mode", choices=["drift", "depth", "budget"], default="drift",
+    ap.add_argument("--mode", choices=["drift", "depth", "budget", "polish"], default="drift",
                     help="drift: exact circuits only, equal-cost moves accepted; depth: minimise (gates, depth); "
-                         "budget: may trade exactness for one gate less and drift back (cgp.c mode 2)")
+                         "budget: may trade exactness for one gate less and drift back (cgp.c mode 2); "
+                         "polish: minimise (gates, -foldable outputs, depth)")
     ap.add_argument("--weight", type=int, default=16, help="budget mode: wrong bits per gate over budget")
     a = ap.parse_args()
     build()
@@ -106,21 +105,21 @@ def main():
     for rnd in range(a.rounds):
         start = current_best()
         for g, c in saved.items():
-            if (len(c["gates"]), depth(c)) < (len(start[g]["gates"]), depth(start[g])):
+            if rank(c) < rank(start[g]):
                 start[g] = c
         tasks = []
         for i in range(max(a.jobs, len(boxes))):
             g = boxes[i % len(boxes)]
-            tasks.append((g, start[g], a.seconds, seed, a.slack, {"drift": 0, "depth": 1, "budget": 2}[a.mode],
+            tasks.append((g, start[g], a.seconds, seed, a.slack, {"drift": 0, "depth": 1, "budget": 2, "polish": 3}[a.mode],
                           a.weight))
             seed += 1
         with ThreadPoolExecutor(a.jobs) as ex:
             for g, sd, found in ex.map(lambda t: run_one(*t), tasks):
                 for c in found:
-                    key = (len(c["gates"]), depth(c))
+                    key = rank(c)
                     old = saved.get(g)
-                    if old is None or key < (len(old["gates"]), depth(old)):
-                        if key < (len(start[g]["gates"]), depth(start[g])) or old is not None:
+                    if old is None or key < rank(old):
+                        if key < rank(start[g]) or old is not None:
                             saved[g] = dict(c, sbox=g, seed=sd)
                             save(saved)
                             print(f"round {rnd}: S{g + 1} -> {len(c['gates'])} gates, depth {depth(c)} "

@@ -22,6 +22,8 @@
  *   above the best count - 1), W = argv[6] (default 16); a child is accepted if its
  *   fitness is no worse, so the search may give up exactness to drop a gate and
  *   then drift back to an exact circuit one gate smaller (printed when found).
+ *   depth_mode = 3: polish -- minimise (gates, -foldable outputs, depth) (a folded
+ *   output saves the round one key IMAD; measured worth about half a gate).
  *   depth_mode = 1: minimise (gates, depth) lexicographically -- a child is accepted
  *   only if it is no worse in either order, and every strictly better circuit is
  *   printed (used to bring a reduced circuit's depth back down: a deeper S-box
@@ -126,6 +128,39 @@ static int depth(const G *g, const uint8_t *act) {
     if (v > best) best = v;
   }
   return best;
+}
+
+/* Outputs whose Feistel XOR can also fold a key mask (tools/gen_tdes.py
+ * fold_producers): an unfused output, or a fused XOR/XNOR join one of whose
+ * operands is a gate with at most two distinct inputs and no other consumer. */
+static int foldable(const G *g, const uint8_t *act) {
+  int uses[6 + MAXN] = {0};
+  for (int k = 0; k < N; k++) {
+    if (!act[k]) continue;
+    const int a = g->in[k][0], b = g->in[k][1], c = g->in[k][2];
+    uses[a]++;
+    if (b != a) uses[b]++;
+    if (c != a && c != b) uses[c]++;
+  }
+  for (int o = 0; o < 4; o++)
+    if (g->otype[o]) {
+      uses[g->ou[o]]++;
+      if (g->ov[o] != g->ou[o]) uses[g->ov[o]]++;
+    }
+  int n = 0;
+  for (int o = 0; o < 4; o++) {
+    if (g->otype[o] == 0) { n++; continue; }
+    if (g->oh[o] != 6 && g->oh[o] != 9) continue;
+    const int sg[2] = {g->ou[o], g->ov[o]};
+    for (int j = 0; j < 2; j++) {
+      const int x = sg[j];
+      if (x < 6) continue;
+      const int k = x - 6, a = g->in[k][0], b = g->in[k][1], c = g->in[k][2];
+      const int distinct = 1 + (b != a) + (c != a && c != b);
+      if (distinct <= 2 && uses[x] == 1) { n++; break; }
+    }
+  }
+  return n;
 }
 
 static void mutate(G *g, uint64_t *rs) {
@@ -248,6 +283,33 @@ int main(int argc, char **argv) {
   fprintf(stderr, "start: %d gates, depth %d\n", pc, pd);
   const clock_t t0 = clock();
   long gen = 0;
+  if (depth_mode == 3) {
+    int pfo = foldable(&p, act), bfo = pfo, bd3 = pd, bc3 = pc;
+    fprintf(stderr, "polish start: %d gates, %d foldable, depth %d\n", pc, pfo, pd);
+    for (;;) {
+      if ((++gen & 0xFFFF) == 0 && (double)(clock() - t0) / CLOCKS_PER_SEC > secs) break;
+      for (int l = 0; l < lambda; l++) {
+        G c = p;
+        mutate(&c, &rs);
+        uint8_t ca[MAXN];
+        const int cc = active(&c, ca);
+        if (cc > pc) continue;
+        if (errors(&c, ca) != 0) continue;
+        const int cfo = foldable(&c, ca), cd = depth(&c, ca);
+        if (cc < pc || cfo > pfo || (cfo == pfo && cd <= pd)) {
+          p = c, pc = cc, pfo = cfo, pd = cd;
+          if (cc < bc3 || (cc == bc3 && (cfo > bfo || (cfo == bfo && cd < bd3)))) {
+            bc3 = cc, bfo = cfo, bd3 = cd;
+            fprintf(stderr, "gen %ld: %d gates, %d foldable, depth %d\n", gen, cc, cfo, cd);
+            print_json(&p);
+          }
+          break;
+        }
+      }
+    }
+    fprintf(stderr, "done: %ld generations\n", gen);
+    return 0;
+  }
   if (depth_mode == 2) {
     int budget = pc - 1;
     int pf = weight;  /* parent fitness: exact, one gate over budget */
