@@ -416,3 +416,17 @@ def test_debug_build_rejects_host_pointers():
     assert res["host_in"] == -1 and res["pinned_in"] == -1 and res["host_out"] == -1
     assert res["split_host_in"] == -1
     assert res["device"] == 0 and res["exact"] is True
+
+
+@pytest.mark.parametrize("keying", list(KEYINGS))
+@pytest.mark.parametrize("mode", [1, 3])
+@pytest.mark.parametrize("decrypt", [False, True])
+def test_keyings_throughput_kernels(tdes, keying, mode, decrypt):
+    """3-, 2- and 1-key through both throughput kernels -- host-folded key
+    operands (mode 1) and device-expanded (mode 3, NEXT-4) -- both directions."""
+    keys = KEYINGS[keying]
+    n = 300 * 1024 + 55
+    p = synthetic.plaintext_bytes(5 * n, n)
+    s = tdes.key_schedule(*keys)
+    got = tdes.ecb_crypt_mode(to_dev(p), s, mode, decrypt=decrypt).cpu().numpy()
+    assert np.array_equal(got, oracle.tdes_ecb(*keys, p, decrypt=decrypt))
