@@ -13,7 +13,7 @@ s = tdes.key_schedule(*synthetic.KEYS_3KEY)
 x = torch.empty(8 * n, dtype=torch.uint8, device="cuda")
 tdes.fill_splitmix64(x)
 y = torch.empty_like(x)
-for mode in (1, 2):                               # throughput and S-box-split kernels
+for mode in (1, 2, 3):                            # throughput (host-folded, device-expanded keys) and split kernels
     tdes.ecb_crypt_mode(x, s, mode, out=y)
     tdes.ecb_crypt_mode(y, s, mode, decrypt=True, out=y)   # in place
 tdes.ecb_encrypt(x[8:8 + 8 * 1000], s, out=y[8:8 + 8 * 1000])   # 8-byte-aligned path
