@@ -163,7 +163,7 @@ def load_searched():
             g = item["sbox"]
             circ = {"gates": item["gates"], "outputs": item["outputs"],
                     "neg": item.get("neg", [0, 0, 0, 0]), "fuse": item.get("fuse") or [None] * 4,
-                    "source": os.path.basename(path)}
+                    "source": os.path.basename(path), "measured": "measured_gain_pct" in item}
             if not verify_circuit(g, circ):
                 print(f"warning: {path} S{g + 1} circuit fails verification; ignored", file=sys.stderr)
                 continue
@@ -184,12 +184,14 @@ def circuit_depth(circ) -> int:
 
 
 def circuit_rank(circ):
-    """Choice among verified circuits of one S-box: fewest gates, then the most
-    outputs that can fold a key mask (each saves the round one key IMAD; measured
-    worth about half a gate), then the lowest depth."""
+    """Choice among verified circuits of one S-box: fewest gates, then one picked by
+    measurement, then the most outputs that can fold a key mask (each saves the
+    round one key IMAD), then the lowest depth."""
     n = normalize_outputs(circ)
     folds = sum(1 for o, f in enumerate(n.get("fuse") or [None] * 4) if f is None or o in fold_producers(n))
-    return (circuit_cost(circ), -folds, circuit_depth(circ))
+    # a circuit chosen by a B200 A/B among equal-cost ones (tools/exp/select_circuits.py)
+    # beats the static tie-breakers
+    return (circuit_cost(circ), 0 if circ.get("measured") else 1, -folds, circuit_depth(circ))
 
 
 def normalize_outputs(circ):

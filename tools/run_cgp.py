@@ -6,7 +6,8 @@ Starting circuits are tools/gen_tdes.py's choice over tools/circuits/*.json (our
 own search results).  Runs are independent processes (one per core), each one
 S-box and seed; every improved circuit is verified exhaustively against the
 S-box table (gen_tdes.verify_circuit) before it is written to
-tools/circuits/lut3_cgp.json (per S-box the fewest gates, then the lowest depth).
+tools/circuits/candidates/lut3_cgp_candidates.json (per S-box the best by
+gen_tdes.circuit_rank); adopted circuits are copied to tools/circuits/lut3_cgp.json.
 
   python tools/run_cgp.py --seconds 600 [--boxes 1,5,7] [--jobs 8] [--slack 6] [--rounds 3]
                           [--mode drift|depth|budget] [--weight 16]
@@ -25,7 +26,10 @@ import gen_tdes  # noqa: E402
 
 SRC = os.path.join(HERE, "sbox_search", "cgp.c")
 BIN = os.path.join(HERE, "sbox_search", "cgp")
-OUT = os.path.join(HERE, "circuits", "lut3_cgp.json")
+# Search output goes to candidates/ (not read by the generator); a circuit moves to
+# circuits/lut3_cgp.json only after an A/B on the GPU (equal-cost circuits differ by
+# up to ~2% in kernel time).
+OUT = os.path.join(HERE, "circuits", "candidates", "lut3_cgp_candidates.json")
 
 
 def build():

@@ -22,6 +22,9 @@
  *   above the best count - 1), W = argv[6] (default 16); a child is accepted if its
  *   fitness is no worse, so the search may give up exactness to drop a gate and
  *   then drift back to an exact circuit one gate smaller (printed when found).
+ *   depth_mode = 4: sample -- neutral drift among exact circuits of at most the
+ *   starting gate count, printing the current circuit every 2^22 generations
+ *   (structurally different equal-cost alternatives, for measured selection).
  *   depth_mode = 3: polish -- minimise (gates, -foldable outputs, depth) (a folded
  *   output saves the round one key IMAD; measured worth about half a gate).
  *   depth_mode = 1: minimise (gates, depth) lexicographically -- a child is accepted
@@ -283,6 +286,20 @@ int main(int argc, char **argv) {
   fprintf(stderr, "start: %d gates, depth %d\n", pc, pd);
   const clock_t t0 = clock();
   long gen = 0;
+  if (depth_mode == 4) {
+    const int cap = pc;
+    for (;;) {
+      if ((++gen & 0xFFFF) == 0 && (double)(clock() - t0) / CLOCKS_PER_SEC > secs) break;
+      if ((gen & 0x3FFFFF) == 0) print_json(&p);
+      G c = p;
+      mutate(&c, &rs);
+      uint8_t ca[MAXN];
+      const int cc = active(&c, ca);
+      if (cc > cap || errors(&c, ca) != 0) continue;
+      p = c;
+    }
+    return 0;
+  }
   if (depth_mode == 3) {
     int pfo = foldable(&p, act), bfo = pfo, bd3 = pd, bc3 = pc;
     fprintf(stderr, "polish start: %d gates, %d foldable, depth %d\n", pc, pfo, pd);
