@@ -34,8 +34,9 @@ import run_cgp  # noqa: E402
 SEL = os.path.join(HERE, "sel")
 
 
-def samples(g, circ, secs, seed):
-    p = subprocess.run([run_cgp.BIN, str(secs), str(seed), "4", "4", "4"], input=run_cgp.to_stdin(g, circ),
+def samples(g, circ, secs, seed, log_every=22):
+    p = subprocess.run([run_cgp.BIN, str(secs), str(seed), "4", "4", "4", str(log_every)],
+                       input=run_cgp.to_stdin(g, circ),
                        capture_output=True, text=True)
     out, seen = [], set()
     for line in p.stdout.splitlines():
@@ -66,7 +67,7 @@ def cmd_build(a):
     cur = gen_tdes.choose_circuits()
     boxes = [int(b) - 1 for b in a.boxes.split(",")]
     with ThreadPoolExecutor(len(boxes)) as ex:
-        got = dict(zip(boxes, ex.map(lambda g: samples(g, cur[g], a.seconds, 1000 + g), boxes)))
+        got = dict(zip(boxes, ex.map(lambda g: samples(g, cur[g], a.seconds, a.seed + g, a.log_every), boxes)))
     tmp = tempfile.mkdtemp(prefix="sel_")
     jobs = [(os.path.join(SEL, "base.so"), base_files, "")]
     manifest = {}
@@ -129,6 +130,8 @@ def main():
     b.add_argument("--k", type=int, default=5)
     b.add_argument("--seconds", type=float, default=40)
     b.add_argument("--jobs", type=int, default=8)
+    b.add_argument("--seed", type=int, default=1000)
+    b.add_argument("--log-every", type=int, default=22, help="sample every 2^L generations (smaller: nearer variants)")
     p = sub.add_parser("pick")
     p.add_argument("results")
     p.add_argument("--min-gain", type=float, default=0.3)

@@ -23,7 +23,8 @@
  *   fitness is no worse, so the search may give up exactness to drop a gate and
  *   then drift back to an exact circuit one gate smaller (printed when found).
  *   depth_mode = 4: sample -- neutral drift among exact circuits of at most the
- *   starting gate count, printing the current circuit every 2^22 generations
+ *   starting gate count, printing the current circuit every 2^L generations
+ *   (L = argv[6], default 22; smaller L = variants closer to the start)
  *   (structurally different equal-cost alternatives, for measured selection).
  *   depth_mode = 3: polish -- minimise (gates, -foldable outputs, depth) (a folded
  *   output saves the round one key IMAD; measured worth about half a gate).
@@ -288,9 +289,10 @@ int main(int argc, char **argv) {
   long gen = 0;
   if (depth_mode == 4) {
     const int cap = pc;
+    const long every = (1L << (argc > 6 ? atoi(argv[6]) : 22)) - 1;
     for (;;) {
       if ((++gen & 0xFFFF) == 0 && (double)(clock() - t0) / CLOCKS_PER_SEC > secs) break;
-      if ((gen & 0x3FFFFF) == 0) print_json(&p);
+      if ((gen & every) == 0) print_json(&p);
       G c = p;
       mutate(&c, &rs);
       uint8_t ca[MAXN];
