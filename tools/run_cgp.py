@@ -96,10 +96,11 @@ def main():
     ap.add_argument("--slack", type=int, default=6)
     ap.add_argument("--rounds", type=int, default=1, help="restart from the improved circuits this often")
     ap.add_argument("--seed", type=int, default=int(time.time()) & 0xFFFF)
-    ap.add_argument("--mode", choices=["drift", "depth", "budget", "polish"], default="drift",
+    ap.add_argument("--mode", choices=["drift", "depth", "budget", "polish", "foldcredit"], default="drift",
                     help="drift: exact circuits only, equal-cost moves accepted; depth: minimise (gates, depth); "
                          "budget: may trade exactness for one gate less and drift back (cgp.c mode 2); "
-                         "polish: minimise (gates, -foldable outputs, depth)")
+                         "polish: minimise (gates, -foldable outputs, depth); "
+                         "foldcredit: minimise gates - foldable outputs (cgp.c mode 5)")
     ap.add_argument("--weight", type=int, default=16, help="budget mode: wrong bits per gate over budget")
     a = ap.parse_args()
     build()
@@ -114,7 +115,7 @@ def main():
         tasks = []
         for i in range(max(a.jobs, len(boxes))):
             g = boxes[i % len(boxes)]
-            tasks.append((g, start[g], a.seconds, seed, a.slack, {"drift": 0, "depth": 1, "budget": 2, "polish": 3}[a.mode],
+            tasks.append((g, start[g], a.seconds, seed, a.slack, {"drift": 0, "depth": 1, "budget": 2, "polish": 3, "foldcredit": 5}[a.mode],
                           a.weight))
             seed += 1
         with ThreadPoolExecutor(a.jobs) as ex:

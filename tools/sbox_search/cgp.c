@@ -22,6 +22,10 @@
  *   above the best count - 1), W = argv[6] (default 16); a child is accepted if its
  *   fitness is no worse, so the search may give up exactness to drop a gate and
  *   then drift back to an exact circuit one gate smaller (printed when found).
+ *   depth_mode = 5: fold credit -- neutral drift on exact circuits minimising
+ *   gates - foldable outputs (a fold saves the round a key IMAD and its loads,
+ *   measured worth about one gate: profiles/r02/circuits_ab.txt), never above the
+ *   starting gate count, depth within 2 of the start; prints every improvement.
  *   depth_mode = 4: sample -- neutral drift among exact circuits of at most the
  *   starting gate count, printing the current circuit every 2^L generations
  *   (L = argv[6], default 22; smaller L = variants closer to the start)
@@ -287,6 +291,33 @@ int main(int argc, char **argv) {
   fprintf(stderr, "start: %d gates, depth %d\n", pc, pd);
   const clock_t t0 = clock();
   long gen = 0;
+  if (depth_mode == 5) {
+    const int g0 = pc;
+    int pcost = pc - foldable(&p, act), bcost = pcost;
+    fprintf(stderr, "fold-credit start: %d gates, cost %d, depth %d\n", pc, pcost, pd);
+    for (;;) {
+      if ((++gen & 0xFFFF) == 0 && (double)(clock() - t0) / CLOCKS_PER_SEC > secs) break;
+      for (int l = 0; l < lambda; l++) {
+        G c = p;
+        mutate(&c, &rs);
+        uint8_t ca[MAXN];
+        const int cc = active(&c, ca);
+        if (cc > g0 || errors(&c, ca) != 0) continue;
+        const int ccost = cc - foldable(&c, ca), cd = depth(&c, ca);
+        if (ccost > pcost || cd > d0 + 2) continue;
+        p = c;
+        pcost = ccost;
+        if (ccost < bcost) {
+          bcost = ccost;
+          fprintf(stderr, "gen %ld: %d gates, cost %d, depth %d\n", gen, cc, ccost, cd);
+          print_json(&p);
+        }
+        break;
+      }
+    }
+    fprintf(stderr, "done: %ld generations, best cost %d\n", gen, bcost);
+    return 0;
+  }
   if (depth_mode == 4) {
     const int cap = pc;
     const long every = (1L << (argc > 6 ? atoi(argv[6]) : 22)) - 1;
