@@ -62,16 +62,6 @@ constexpr int kTileBlocks = kGroupBlocks * kWords;  // per warp
 #define TDES_ROUND_UNROLL 2
 #endif
 constexpr int kRoundUnroll3 = TDES_ROUND_UNROLL;
-// Where the per-thread key operand k of the IMAD key XOR is read from (3DES):
-// 0 = the launch parameters (ptxas emits LDC.64 plus an IMAD.U32 address copy
-//     per load), 1 = a shared-memory copy made at CTA start (one broadcast
-//     LDS.128 per 4 key bits).  s stays a uniform LDCU operand either way.
-// Measured on B200, 1 GiB: 358 -> 370 GB/s for 1; s and k both from shared
-// memory: 348 GB/s.
-#ifndef TDES_KSMEM
-#define TDES_KSMEM 1
-#endif
-constexpr int kKeySmem = TDES_KSMEM;
 // TMA-staged loads: each warp's next 8 KiB tile is fetched into a per-warp
 // shared-memory buffer by one cp.async.bulk (completion on a per-warp mbarrier)
 // while the warp computes the current tile, hiding the HBM latency at tile start.
@@ -90,33 +80,47 @@ constexpr unsigned kTileBytes = kTileBlocks * 8u;
 // the uniform datapath).
 constexpr uint32_t kMulhiC = 0x7FFFFFFFu;
 
-// Launch-parameter key material, consumption order (round, E-bit):
-// s = k | 1 (+1 or -1) where k is the subkey bit's all-ones / all-zeros lane
-// mask; x ^ k = x * s + k is one IMAD (tdes_gen::kxor).  s is read as a uniform
-// operand; k is copied to shared memory at CTA start (kKeySmem).
+// Key material, consumption order (round, E-bit): s = k | 1 (+1 or -1) where k
+// is the subkey bit's all-ones / all-zeros lane mask; x ^ k = x * s + k is one
+// IMAD (tdes_gen::kxor).
 //
-// Mask folding: the planes carry pending uniform masks that the
-// host tracks (build_masks), so s/k are the combined "pending mask ^ key bit"
-// operands of the E-positions that still need a key IMAD (tdes_gen::kKeySlots of
-// 48), d are the masks the unfused outputs fold into their planes, fix the
-// operands that prime round A's free positions before round 0 and after each
-// stage-boundary swap, fin the final unmasking of all 64 planes.
+// Mask folding: the planes carry pending uniform masks, so s/k are
+// the combined "pending mask ^ key bit" operands of the E-positions that still
+// need a key IMAD (tdes_gen::kKeySlots of 48), d are the masks the unfused
+// outputs fold into their planes, fix the operands that prime round A's free
+// positions before round 0 and after each stage-boundary swap, fin the final
+// unmasking of all 64 planes.  RoundMasks is the whole set as the host computes
+// it (build_masks; tdes_fold_operands returns it).
 template <int NROUNDS>
 struct alignas(16) RoundMasks {
   uint32_t s[NROUNDS][tdes_gen::kKeyStride];
-  uint32_t k[NROUNDS][tdes_gen::kKeyStride];  // not read by the MULHI key XOR
+  uint32_t k[NROUNDS][tdes_gen::kKeyStride];
   uint32_t d[NROUNDS][tdes_gen::kDeltaStride];
   uint32_t fix_s[3][tdes_gen::kDeltaStride], fix_k[3][tdes_gen::kDeltaStride];
   uint32_t fin_s[64], fin_k[64];
 };
 
-// The split (latency) kernel takes the subkeys bit-packed (one 48-bit word per
-// round, 384 B for 3DES) and expands its own s table in shared memory: it is
-// latency bound, and launch cost grows with the parameter size
-// (tools/exp/param_lat.cu).
+// The subkeys bit-packed, one 48-bit word per round (384 B for 3DES): the launch
+// parameter of the split kernel and of the device-key throughput kernel, which
+// expand every operand they need from it on the device.
 template <int NROUNDS>
 struct RoundKeys {
   uint64_t k[NROUNDS];  // bit 47 - b = subkey bit b (E position b), consumption order
+};
+
+// The throughput kernel's launch parameters (SKeys): only the s operands, which
+// the round reads as uniform operands -- and the uniform datapath loads only from
+// the constant bank, i.e. from the launch parameters -- plus the packed subkeys,
+// from which each CTA expands k, d, the fix-ups and the unmask into shared memory
+// (expand_keys).  7.9 KB for 3DES instead of the 18 KB RoundMasks of round 1,
+// whose k/d copy from the constant bank cost each CTA ~4 us at start
+// (tools/exp/trace_prologue.py).
+template <int NROUNDS>
+struct alignas(16) SKeys {
+  uint32_t s[NROUNDS][tdes_gen::kKeyStride];
+  uint32_t fix_s[3][tdes_gen::kDeltaStride], fix_k[3][tdes_gen::kDeltaStride];
+  uint32_t fin_s[64], fin_k[64];
+  uint64_t k[NROUNDS];
 };
 
 // Mask folding, symbolically.  The planes' pending masks M are
@@ -208,16 +212,6 @@ __device__ __forceinline__ const OpRefs<NSTAGES>& refs_dev() {
   if constexpr (NSTAGES == 3) return kDevRefs3; else return kDevRefs1;
 }
 
-// Key-XOR form per variant (tdes_gen::kxor).  With k read from the launch
-// parameters, rebuilding k from s (MULHI) was 1.9x faster for single DES (ptxas
-// emitted 32-bit per-thread LDCs that saturated the ADU pipe) and 9% slower for
-// 3DES.  With k from the shared-memory copy (TDES_KSMEM=1) the loaded form wins
-// for both (B200, 1 GiB: DES 828 -> 944 GB/s).
-#ifndef TDES_DES_MULHI
-#define TDES_DES_MULHI 0
-#endif
-template <int NSTAGES>
-constexpr bool kUseMulhi = NSTAGES == 1 && (TDES_DES_MULHI || !TDES_KSMEM);
 
 // x >> s as the high word of x * 2^(32-s): IMAD.HI on the FMA pipe instead of
 // SHF on the integer ALU pipe (the kernel's bound).  Left shifts already
@@ -471,64 +465,31 @@ __device__ __forceinline__ void crypt_tile(const uint2* in, uint2* out, size_t b
 }
 
 // ---- key operand sources of the throughput kernel ----
-// ParamKeys: the host-folded operands (RoundMasks, build_masks) are the launch
-// parameters; s is read as a uniform operand (LDCU) straight from them, k and d
-// from a shared-memory copy the CTA makes at start (one broadcast LDS.128 per
-// four values).  18 KB of parameters for 3DES.
-template <int NSTAGES>
-struct ParamKeys {
-  const RoundMasks<16 * NSTAGES>& mk;
-  const uint4* ksm;  // per round: kKv k vectors, then kDv d vectors
+// Both variants expand the packed subkeys on the device, at CTA start, into the
+// operands the rounds read from shared memory (expand_keys).  They differ in s:
+//   ParamKeys (WITH_S = false; the launch parameters are SKeys): s is read in the
+//     round as a uniform operand (LDCU) straight from the launch parameters, k and
+//     d from the shared-memory table with broadcast LDS.128 (4 values each);
+//   DevKeys (WITH_S = true, NEXT-4; the launch parameters are the 384-byte
+//     RoundKeys): s comes from the shared-memory table as well, into vector
+//     registers (IMAD x * s + k with every operand a vector register) -- 6.5%
+//     slower on long launches, faster to start.
+// Table layout per round: [s (kKv uint4, DevKeys only) | k (kKv) | d (kDv)], then
+// the fix-up and unmask words ff = fix_s[3][kDeltaStride] fix_k[3][kDeltaStride]
+// fin_s[64] fin_k[64].
+template <int NSTAGES, bool WITH_S>
+struct KeyTable {
   static constexpr int kKv = tdes_gen::kKeyStride / 4, kDv = tdes_gen::kDeltaStride / 4;
-  template <class V>
-  __device__ __forceinline__ void fixup(V (&P)[64], int b, uint32_t c) const {
-    tdes_gen::fold_fixup_A<kUseMulhi<NSTAGES>>(P, mk.fix_s[b], mk.fix_k[b], c);
-  }
-  template <class V>
-  __device__ __forceinline__ void two_rounds(V (&P)[64], int r, uint32_t c) const {
-    if (kKeySmem == 0 || kUseMulhi<NSTAGES>) {
-      tdes_gen::round_A<kUseMulhi<NSTAGES>>(P, mk.s[r], mk.k[r], mk.d[r], c);
-      tdes_gen::round_B<kUseMulhi<NSTAGES>>(P, mk.s[r + 1], mk.k[r + 1], mk.d[r + 1], c);
-    } else {  // k and d from the shared-memory table: [round][k | d] as uint4
-      const uint4* t0 = ksm + (kKv + kDv) * r;
-      const uint4* t1 = ksm + (kKv + kDv) * (r + 1);
-      // s as uint2 pairs: every uniform load is 64-bit, also for an odd slot count
-      const uint2* s0 = reinterpret_cast<const uint2*>(mk.s[r]);
-      const uint2* s1 = reinterpret_cast<const uint2*>(mk.s[r + 1]);
-      tdes_gen::round_A<false>(P, s0, t0, t0 + kKv, c);
-      tdes_gen::round_B<false>(P, s1, t1, t1 + kKv, c);
-    }
-  }
-  template <class V>
-  __device__ __forceinline__ void unmask(V (&P)[64], uint32_t c) const {
-    tdes_gen::fold_unmask<kUseMulhi<NSTAGES>>(P, mk.fin_s, mk.fin_k, c);
-  }
-};
-
-// DevKeys (NEXT-4): the launch carries only the 48 (16) packed subkeys in
-// consumption order (RoundKeys, 384 B); each CTA expands them at start into every
-// operand the rounds use -- s, k, d, fix-ups, final unmask -- as key(a) ^ key(b)
-// over the compile-time reference pairs OpRefs (expand_keys below), all in shared
-// memory.  The round reads s and k with broadcast LDS.128 into vector registers
-// (IMAD x * s + k with every operand a vector register).
-template <int NSTAGES>
-struct DevKeys {
-  static constexpr int kKv = tdes_gen::kKeyStride / 4, kDv = tdes_gen::kDeltaStride / 4;
-  static constexpr int kSt = 2 * kKv + kDv;  // uint4 per round: s | k | d
+  static constexpr int kSt = (WITH_S ? 2 : 1) * kKv + kDv;  // uint4 per round
+  static constexpr int kS = 0, kK = WITH_S ? kKv : 0, kD = kK + kKv;  // offsets in a round
   static constexpr int kTabVecs = kSt * 16 * NSTAGES;
   static constexpr int kFixFinWords = 2 * 3 * tdes_gen::kDeltaStride + 2 * 64;
+  static constexpr int kVecs = kTabVecs + kFixFinWords / 4;
   const uint4* tab;
-  const uint32_t* ff;  // fix_s[3][kDeltaStride] fix_k[3][kDeltaStride] fin_s[64] fin_k[64]
+  const uint32_t* ff;
   template <class V>
   __device__ __forceinline__ void fixup(V (&P)[64], int b, uint32_t c) const {
     tdes_gen::fold_fixup_A<false>(P, ff + tdes_gen::kDeltaStride * b, ff + tdes_gen::kDeltaStride * (3 + b), c);
-  }
-  template <class V>
-  __device__ __forceinline__ void two_rounds(V (&P)[64], int r, uint32_t c) const {
-    const uint4* t0 = tab + kSt * r;
-    const uint4* t1 = tab + kSt * (r + 1);
-    tdes_gen::round_A<false>(P, t0, t0 + kKv, t0 + 2 * kKv, c);
-    tdes_gen::round_B<false>(P, t1, t1 + kKv, t1 + 2 * kKv, c);
   }
   template <class V>
   __device__ __forceinline__ void unmask(V (&P)[64], uint32_t c) const {
@@ -536,45 +497,72 @@ struct DevKeys {
   }
 };
 
-// NSTAGES = 3: fused 3DES (48 rounds); NSTAGES = 1: single DES (16 rounds).
-// Work distribution: CTA c owns the contiguous tile range
-// [ntiles*c/grid, ntiles*(c+1)/grid); its warps claim tiles one at a time
-// from a shared-memory counter.  Warps of one SM progress at very different
-// rates under the hardware's warp arbitration, so a static per-warp split
-// leaves the SM waiting on its slowest warp (measured: 1.6-2x slower).
-// Launch parameters of the key material: RoundMasks (host-folded, 18 KB for
-// 3DES) or RoundKeys (packed subkeys, 384 B; DEVKEYS).
-template <int NSTAGES, bool DEVKEYS>
-using KeyParam = std::conditional_t<DEVKEYS, RoundKeys<16 * NSTAGES>, RoundMasks<16 * NSTAGES>>;
-
-template <int NSTAGES, bool DEVKEYS>
-constexpr int kKeySmemVecs =
-    DEVKEYS ? DevKeys<NSTAGES>::kTabVecs + DevKeys<NSTAGES>::kFixFinWords / 4
-            : (kKeySmem == 0 || kUseMulhi<NSTAGES> ? 1 : (ParamKeys<NSTAGES>::kKv + ParamKeys<NSTAGES>::kDv) * 16 * NSTAGES);
-
-// DevKeys prologue: every operand word = key(a) ^ key(b) over OpRefs, the key
-// bits taken from the packed subkeys (bit 47 - pos of round r = E-position pos).
 template <int NSTAGES>
-__device__ __forceinline__ void expand_keys(const RoundKeys<16 * NSTAGES>& kp, uint4* smem) {
-  using DK = DevKeys<NSTAGES>;
+struct ParamKeys {
+  using T = KeyTable<NSTAGES, false>;
+  const SKeys<16 * NSTAGES>& kp;
+  T t;
+  template <class V>
+  __device__ __forceinline__ void fixup(V (&P)[64], int b, uint32_t c) const {
+    tdes_gen::fold_fixup_A<false>(P, kp.fix_s[b], kp.fix_k[b], c);
+  }
+  template <class V>
+  __device__ __forceinline__ void unmask(V (&P)[64], uint32_t c) const {
+    tdes_gen::fold_unmask<false>(P, kp.fin_s, kp.fin_k, c);
+  }
+  template <class V>
+  __device__ __forceinline__ void two_rounds(V (&P)[64], int r, uint32_t c) const {
+    const uint4* t0 = t.tab + T::kSt * r;
+    const uint4* t1 = t.tab + T::kSt * (r + 1);
+    // s as uint2 pairs: every uniform load is 64-bit, also for an odd slot count
+    const uint2* s0 = reinterpret_cast<const uint2*>(kp.s[r]);
+    const uint2* s1 = reinterpret_cast<const uint2*>(kp.s[r + 1]);
+    tdes_gen::round_A<false>(P, s0, t0 + T::kK, t0 + T::kD, c);
+    tdes_gen::round_B<false>(P, s1, t1 + T::kK, t1 + T::kD, c);
+  }
+};
+
+template <int NSTAGES>
+struct DevKeys : KeyTable<NSTAGES, true> {
+  using T = KeyTable<NSTAGES, true>;
+  __device__ DevKeys(const uint4* tab, const uint32_t* ff) : T{tab, ff} {}
+  template <class V>
+  __device__ __forceinline__ void two_rounds(V (&P)[64], int r, uint32_t c) const {
+    const uint4* t0 = this->tab + T::kSt * r;
+    const uint4* t1 = this->tab + T::kSt * (r + 1);
+    tdes_gen::round_A<false>(P, t0 + T::kS, t0 + T::kK, t0 + T::kD, c);
+    tdes_gen::round_B<false>(P, t1 + T::kS, t1 + T::kK, t1 + T::kD, c);
+  }
+};
+
+// Launch parameters of the key material (DEVKEYS: the packed subkeys only).
+template <int NSTAGES, bool DEVKEYS>
+using KeyParam = std::conditional_t<DEVKEYS, RoundKeys<16 * NSTAGES>, SKeys<16 * NSTAGES>>;
+
+// The prologue's expansion: every operand word = key(a) ^ key(b) over OpRefs, the
+// key bits taken from the packed subkeys (first copied to shared memory; bit
+// 47 - pos of round r = E-position pos).
+template <int NSTAGES, bool WITH_S>
+__device__ __forceinline__ void expand_keys(const uint64_t* kbits, uint4* smem) {
+  using KT = KeyTable<NSTAGES, WITH_S>;
   using namespace tdes_gen;
   constexpr int NR = 16 * NSTAGES;
   const OpRefs<NSTAGES>& o = refs_dev<NSTAGES>();
   auto bit = [&](uint16_t ref) -> uint32_t {
-    return ref == kNoRef ? 0u : 0u - (uint32_t)((kp.k[ref / 48] >> (47 - ref % 48)) & 1u);
+    return ref == kNoRef ? 0u : 0u - (uint32_t)((kbits[ref / 48] >> (47 - ref % 48)) & 1u);
   };
   uint32_t* t32 = reinterpret_cast<uint32_t*>(smem);
   for (int i = threadIdx.x; i < NR * kKeyStride; i += blockDim.x) {
     const int r = i / kKeyStride, q = i % kKeyStride;
     const uint32_t v = bit(o.sk[r][q][0]) ^ bit(o.sk[r][q][1]);
-    t32[4 * (r * DK::kSt) + q] = v | 1u;        // s
-    t32[4 * (r * DK::kSt + DK::kKv) + q] = v;   // k
+    if (WITH_S) t32[4 * (r * KT::kSt + KT::kS) + q] = v | 1u;  // s
+    t32[4 * (r * KT::kSt + KT::kK) + q] = v;                   // k
   }
   for (int i = threadIdx.x; i < NR * kDeltaStride; i += blockDim.x) {
     const int r = i / kDeltaStride, u = i % kDeltaStride;
-    t32[4 * (r * DK::kSt + 2 * DK::kKv) + u] = bit(o.d[r][u][0]) ^ bit(o.d[r][u][1]);
+    t32[4 * (r * KT::kSt + KT::kD) + u] = bit(o.d[r][u][0]) ^ bit(o.d[r][u][1]);
   }
-  uint32_t* ff = t32 + 4 * DK::kTabVecs;
+  uint32_t* ff = t32 + 4 * KT::kTabVecs;
   for (int i = threadIdx.x; i < 3 * kDeltaStride; i += blockDim.x) {
     const int b = i / kDeltaStride, t = i % kDeltaStride;
     const uint32_t v = bit(o.fix[b][t][0]) ^ bit(o.fix[b][t][1]);
@@ -589,8 +577,8 @@ __device__ __forceinline__ void expand_keys(const RoundKeys<16 * NSTAGES>& kp, u
 }
 
 // NSTAGES = 3: fused 3DES (48 rounds); NSTAGES = 1: single DES (16 rounds).
-// DEVKEYS: key operands expanded on the device from the packed subkeys (DevKeys)
-// instead of host-folded launch parameters (ParamKeys).
+// DEVKEYS: s from the shared-memory table too (DevKeys) instead of the launch
+// parameters (ParamKeys).
 // Work distribution: CTA c owns the contiguous tile range
 // [ntiles*c/grid, ntiles*(c+1)/grid); its warps claim tiles one at a time
 // from a shared-memory counter.  Warps of one SM progress at very different
@@ -600,29 +588,25 @@ template <int NSTAGES, bool VEC4, bool DEVKEYS>
 __global__ void __launch_bounds__(kThreads, kMinCtasPerSm)
 tdes_ecb_kernel(const uint2* in, uint2* out, size_t nblocks,
                 const __grid_constant__ KeyParam<NSTAGES, DEVKEYS> kp, uint32_t c) {
+  using KT = KeyTable<NSTAGES, DEVKEYS>;
   __shared__ unsigned int next_tile;
-  // shared-memory key table: ParamKeys per round the kKeySlots k operands then the
-  // unfused-output masks d (9 KiB for 3DES); DevKeys every operand (18 KiB)
-  __shared__ uint4 ksm[kKeySmemVecs<NSTAGES, DEVKEYS>];
+  __shared__ uint64_t kbits[16 * NSTAGES];
+  __shared__ uint4 ksm[KT::kVecs];  // the key table (9.9 KiB for 3DES; 17.4 KiB with s)
   const unsigned lane = threadIdx.x & 31u;
+  const unsigned warp = threadIdx.x >> 5;
   const size_t ntiles = (nblocks + kTileBlocks - 1) / kTileBlocks;
   const size_t lo = ntiles * blockIdx.x / gridDim.x;
   const size_t hi = ntiles * (blockIdx.x + 1) / gridDim.x;
   if (threadIdx.x == 0) next_tile = 0;
-  if constexpr (DEVKEYS) {
-    expand_keys<NSTAGES>(kp, ksm);
-  } else if (kKeySmem != 0 && !kUseMulhi<NSTAGES>) {
-    constexpr int kKv = ParamKeys<NSTAGES>::kKv, kDv = ParamKeys<NSTAGES>::kDv;
-    const uint4* k4 = reinterpret_cast<const uint4*>(&kp.k[0][0]);
-    const uint4* d4 = reinterpret_cast<const uint4*>(&kp.d[0][0]);
-    for (int i = threadIdx.x; i < kKeySmemVecs<NSTAGES, false>; i += blockDim.x) {
-      const int r = i / (kKv + kDv), q = i % (kKv + kDv);
-      ksm[i] = q < kKv ? k4[r * kKv + q] : d4[r * kDv + q - kKv];
-    }
+  // packed subkeys -> shared memory (warp-uniform parameter loads), then expand
+  for (int r = (int)warp; r < 16 * NSTAGES; r += kWarps) {
+    const uint64_t v = kp.k[r];
+    if (lane == 0) kbits[r] = v;
   }
+  __syncthreads();
+  expand_keys<NSTAGES, DEVKEYS>(kbits, ksm);
   extern __shared__ uint4 tma_buf[];  // kTma: [kWarps][kTileBytes / 16], dynamic
   __shared__ uint64_t tma_bar[kWarps];
-  const unsigned warp = threadIdx.x >> 5;
   uint4* buf = tma_buf + warp * (kTileBytes / 16);
   if (kTma && lane == 0) mbar_init(&tma_bar[warp]);
   if (kTma) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -636,10 +620,11 @@ tdes_ecb_kernel(const uint2* in, uint2* out, size_t nblocks,
   auto stageable = [&](size_t t) { return kTma && VEC4 && t < hi && (t + 1) * kTileBlocks <= nblocks; };
   using KV = std::conditional_t<DEVKEYS, DevKeys<NSTAGES>, ParamKeys<NSTAGES>>;
   const KV kv = [&]() {
+    const uint32_t* ff = reinterpret_cast<const uint32_t*>(ksm + KT::kTabVecs);
     if constexpr (DEVKEYS)
-      return KV{ksm, reinterpret_cast<const uint32_t*>(ksm + DevKeys<NSTAGES>::kTabVecs)};
+      return KV(ksm, ff);
     else
-      return KV{kp, ksm};
+      return KV{kp, KeyTable<NSTAGES, false>{ksm, ff}};
   }();
   size_t tile = claim();
   bool staged = stageable(tile);
@@ -934,28 +919,6 @@ void build_masks(const uint32_t (*masks)[48], RoundMasks<16 * NSTAGES>& mk) {
   }
 }
 
-// build_masks costs ~10 us of host time per call; launches with the same key
-// material (the common case: one key, many launches) reuse the result.  Two
-// entries per thread and variant, so alternating encrypt/decrypt also hits.
-template <int NSTAGES>
-const RoundMasks<16 * NSTAGES>& cached_masks(const uint32_t (*masks)[48]) {
-  struct Entry {
-    uint32_t key[16 * NSTAGES][48];
-    RoundMasks<16 * NSTAGES> mk;
-    bool valid = false;
-  };
-  thread_local Entry cache[2];
-  thread_local int next = 0;
-  for (Entry& e : cache)
-    if (e.valid && memcmp(e.key, masks, sizeof e.key) == 0) return e.mk;
-  Entry& e = cache[next];
-  next ^= 1;
-  memcpy(e.key, masks, sizeof e.key);
-  build_masks<NSTAGES>(masks, e.mk);
-  e.valid = true;
-  return e.mk;
-}
-
 // The consumption-order key masks packed one 48-bit word per round (bit 47 - b =
 // E-position b): the 384-byte launch parameter of the split kernel and of the
 // device-key throughput kernel.
@@ -969,6 +932,37 @@ RoundKeys<16 * NSTAGES> pack_keys(const uint32_t (*masks)[48]) {
   }
   return ms;
 }
+
+// build_masks costs ~10 us of host time per call; launches with the same key
+// material (the common case: one key, many launches) reuse the result.  Two
+// entries per thread and variant, so alternating encrypt/decrypt also hits.
+template <int NSTAGES>
+const SKeys<16 * NSTAGES>& cached_skeys(const uint32_t (*masks)[48]) {
+  struct Entry {
+    uint32_t key[16 * NSTAGES][48];
+    SKeys<16 * NSTAGES> sk;
+    bool valid = false;
+  };
+  thread_local Entry cache[2];
+  thread_local int next = 0;
+  for (Entry& e : cache)
+    if (e.valid && memcmp(e.key, masks, sizeof e.key) == 0) return e.sk;
+  Entry& e = cache[next];
+  next ^= 1;
+  memcpy(e.key, masks, sizeof e.key);
+  RoundMasks<16 * NSTAGES> mk;
+  build_masks<NSTAGES>(masks, mk);
+  memcpy(e.sk.s, mk.s, sizeof e.sk.s);
+  memcpy(e.sk.fix_s, mk.fix_s, sizeof e.sk.fix_s);
+  memcpy(e.sk.fix_k, mk.fix_k, sizeof e.sk.fix_k);
+  memcpy(e.sk.fin_s, mk.fin_s, sizeof e.sk.fin_s);
+  memcpy(e.sk.fin_k, mk.fin_k, sizeof e.sk.fin_k);
+  const RoundKeys<16 * NSTAGES> pk = pack_keys<NSTAGES>(masks);
+  memcpy(e.sk.k, pk.k, sizeof e.sk.k);
+  e.valid = true;
+  return e.sk;
+}
+
 
 template <int NSTAGES, bool DEVKEYS>
 cudaError_t launch_throughput(const KeyParam<NSTAGES, DEVKEYS>& kp, const uint2* pin, uint2* pout, size_t nblocks,
@@ -1020,7 +1014,7 @@ int launch(const uint32_t (*masks)[48], const void* in, void* out, size_t nblock
   if (mode == 3 || (mode == 0 && ngroups <= kDevKeysMaxTiles))
     e = launch_throughput<NSTAGES, true>(pack_keys<NSTAGES>(masks), pin, pout, nblocks, vec4, dev, stream);
   else
-    e = launch_throughput<NSTAGES, false>(cached_masks<NSTAGES>(masks), pin, pout, nblocks, vec4, dev, stream);
+    e = launch_throughput<NSTAGES, false>(cached_skeys<NSTAGES>(masks), pin, pout, nblocks, vec4, dev, stream);
   if (e != cudaSuccess) return cuda_fail(e);
   return TDES_OK;
 }
