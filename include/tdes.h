@@ -76,13 +76,13 @@ int tdes_key_schedule(const uint8_t k1[8], const uint8_t k2[8], const uint8_t k3
  * device, enqueued on `stream` (asynchronous; kernel faults surface at the
  * caller's next synchronize).
  *   s       host pointer to a schedule from tdes_key_schedule; what the kernel
- *           needs of it is copied into the launch parameters (the host-folded key
- *           operands, or the 48 packed subkeys that the kernel expands on the
- *           device), so *s may be freed or changed as soon as the call returns.
+ *           needs of it is copied into the launch parameters (the 48 packed
+ *           subkeys, which each CTA expands into its key operands on the device,
+ *           plus the uniform-path s operands), so *s may be freed or changed as
+ *           soon as the call returns.
  * Kernel choice (automatic, by launch size in 1024-block tiles): <= 296 tiles the
- * S-box-split latency kernel, <= 768 the throughput kernel with device-side key
- * expansion, above that the throughput kernel with host-folded key operands
- * (tdes_ecb_crypt_mode in tdes_bench.h forces one).  All produce identical output.
+ * S-box-split latency kernel, above that the throughput kernel (tdes_ecb_crypt_mode
+ * in tdes_bench.h forces one).  All produce identical output.
  *   in,out  device pointers (current device), 8-byte aligned; in == out (in
  *           place) is allowed, any other overlap is TDES_ERR_OVERLAP.  16-byte
  *           alignment of both selects 128-bit loads/stores.

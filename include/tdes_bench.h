@@ -48,11 +48,13 @@ int tdes_lop3_peak(uint32_t *dev_sink, int grid, int cta, int iters, uint64_t *o
 /* 3DES ECB with an explicit kernel choice (for measurement and tests):
  *   mode 0  automatic (what tdes_ecb_encrypt/decrypt do: the S-box-split latency
  *           kernel for small launches, the throughput kernel otherwise)
- *   mode 1  throughput kernel (32 blocks per thread, one warp per 1024-block tile)
+ *   mode 1  throughput kernel (32 blocks per thread, one warp per 1024-block tile;
+ *           s operands in the launch parameters, k/d expanded on the device)
  *   mode 2  S-box-split latency kernel (8 warps per tile, one S-box per warp)
- *   mode 3  throughput kernel with device-side key expansion: the launch carries
- *           only the 48 packed 48-bit subkeys (384 B); every CTA expands them into
- *           the folded key operands in shared memory at start (NEXT-4)
+ *   mode 3  throughput kernel with all key operands expanded on the device: the
+ *           launch carries only the 48 packed 48-bit subkeys (384 B); every CTA
+ *           expands them into every folded key operand, s included, in shared
+ *           memory at start (NEXT-4's pure device path; slower on long launches)
  * Same arguments and errors as tdes_ecb_encrypt; decrypt 0/1. */
 int tdes_ecb_crypt_mode(const tdes_schedule *s, int decrypt, const void *in, void *out,
                         size_t nblocks, int mode, tdes_stream_t stream);

@@ -597,7 +597,22 @@ tdes_ecb_kernel(const uint2* in, uint2* out, size_t nblocks,
   const size_t ntiles = (nblocks + kTileBlocks - 1) / kTileBlocks;
   const size_t lo = ntiles * blockIdx.x / gridDim.x;
   const size_t hi = ntiles * (blockIdx.x + 1) / gridDim.x;
-  if (threadIdx.x == 0) next_tile = 0;
+  extern __shared__ uint4 tma_buf[];  // kTma: [kWarps][kTileBytes / 16], dynamic
+  __shared__ uint64_t tma_bar[kWarps];
+  uint4* buf = tma_buf + warp * (kTileBytes / 16);
+  // a tile is staged by TMA when it is full (16-byte aligned, VEC4 path)
+  auto stageable = [&](size_t t) { return kTma && VEC4 && t < hi && (t + 1) * kTileBlocks <= nblocks; };
+  // First tiles are assigned statically (warp w: lo + w) and their TMA copies are
+  // issued before the key expansion, so the HBM latency of the first load overlaps
+  // the prologue; later tiles come from the shared counter (starting at kWarps).
+  if (threadIdx.x == 0) next_tile = kWarps;
+  size_t tile = lo + warp;
+  bool staged = stageable(tile);
+  if (kTma && lane == 0) {
+    mbar_init(&tma_bar[warp]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (staged) tma_load(buf, in + tile * kTileBlocks, kTileBytes, &tma_bar[warp]);
+  }
   // packed subkeys -> shared memory (warp-uniform parameter loads), then expand
   for (int r = (int)warp; r < 16 * NSTAGES; r += kWarps) {
     const uint64_t v = kp.k[r];
@@ -605,19 +620,12 @@ tdes_ecb_kernel(const uint2* in, uint2* out, size_t nblocks,
   }
   __syncthreads();
   expand_keys<NSTAGES, DEVKEYS>(kbits, ksm);
-  extern __shared__ uint4 tma_buf[];  // kTma: [kWarps][kTileBytes / 16], dynamic
-  __shared__ uint64_t tma_bar[kWarps];
-  uint4* buf = tma_buf + warp * (kTileBytes / 16);
-  if (kTma && lane == 0) mbar_init(&tma_bar[warp]);
-  if (kTma) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
   auto claim = [&]() -> size_t {
     unsigned t = 0;
     if (lane == 0) t = atomicAdd(&next_tile, 1u);
     return lo + __shfl_sync(0xffffffffu, t, 0);
   };
-  // a tile is staged by TMA when it is full (16-byte aligned, VEC4 path)
-  auto stageable = [&](size_t t) { return kTma && VEC4 && t < hi && (t + 1) * kTileBlocks <= nblocks; };
   using KV = std::conditional_t<DEVKEYS, DevKeys<NSTAGES>, ParamKeys<NSTAGES>>;
   const KV kv = [&]() {
     const uint32_t* ff = reinterpret_cast<const uint32_t*>(ksm + KT::kTabVecs);
@@ -626,9 +634,6 @@ tdes_ecb_kernel(const uint2* in, uint2* out, size_t nblocks,
     else
       return KV{kp, KeyTable<NSTAGES, false>{ksm, ff}};
   }();
-  size_t tile = claim();
-  bool staged = stageable(tile);
-  if (staged && lane == 0) tma_load(buf, in + tile * kTileBlocks, kTileBytes, &tma_bar[warp]);
   uint32_t phase = 0;
   while (tile < hi) {
     size_t next = hi;
@@ -883,13 +888,12 @@ int check_buffers(const void* in, const void* out, size_t nblocks) {
 // 1024-block tiles, the throughput kernel above (measured crossover).
 constexpr size_t kSplitMaxTiles = 296;
 constexpr size_t kSplitSpecMaxTiles = 16;  // the S-box-specialised split kernel (tdes_split_kernel<., true>)
-// Auto mode: the throughput kernel with device-expanded key operands (mode 3)
-// up to this many tiles, the host-folded one (mode 1) above.  Its 384-byte
-// launch parameters start ~2 us sooner than the 18 KB block, but its s operands
-// come from shared memory instead of the uniform path, which costs 6.5% on long
-// launches (B200, tools/exp/size_timing.py: 2^19 blocks 24.7 -> 23.3 us back to
-// back, 2^20 equal, 2^21 59.8 -> 61.6 us, 1 GiB 2792 -> 2983 us).
-constexpr size_t kDevKeysMaxTiles = 768;
+// Auto mode uses the throughput kernel whose s operands stay in the launch
+// parameters (mode 1) above kSplitMaxTiles.  (Until its prologue expanded k and d
+// on the device and issued the first tile's TMA copy before that expansion, the
+// all-device-keys variant, mode 3, started ~2 us sooner and was used up to 768
+// tiles; now mode 1 is as fast or faster at every size: tools/exp/size_timing.py,
+// profiles/sizes_r02.txt.)
 
 // Host: the operand words for key masks `masks` (consumption order, 0 / ~0).
 template <int NSTAGES>
@@ -1011,7 +1015,7 @@ int launch(const uint32_t (*masks)[48], const void* in, void* out, size_t nblock
   }
   const uint2* pin = static_cast<const uint2*>(in);
   uint2* pout = static_cast<uint2*>(out);
-  if (mode == 3 || (mode == 0 && ngroups <= kDevKeysMaxTiles))
+  if (mode == 3)
     e = launch_throughput<NSTAGES, true>(pack_keys<NSTAGES>(masks), pin, pout, nblocks, vec4, dev, stream);
   else
     e = launch_throughput<NSTAGES, false>(cached_skeys<NSTAGES>(masks), pin, pout, nblocks, vec4, dev, stream);
