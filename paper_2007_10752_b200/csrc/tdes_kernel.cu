@@ -540,39 +540,100 @@ template <int NSTAGES, bool DEVKEYS>
 using KeyParam = std::conditional_t<DEVKEYS, RoundKeys<16 * NSTAGES>, SKeys<16 * NSTAGES>>;
 
 // The prologue's expansion: every operand word = key(a) ^ key(b) over OpRefs, the
-// key bits taken from the packed subkeys (first copied to shared memory; bit
-// 47 - pos of round r = E-position pos).
-template <int NSTAGES, bool WITH_S>
-__device__ __forceinline__ void expand_keys(const uint64_t* kbits, uint4* smem) {
-  using KT = KeyTable<NSTAGES, WITH_S>;
+// key bits taken from the packed subkeys (bit 47 - pos of round r = E-position pos).
+// Two phases, so the reference-pair loads (global memory, L2) overlap the copy of
+// the packed subkeys into shared memory: load_refs issues every load this thread
+// needs at once (compile-time trip counts over kThreads threads), expand_keys
+// combines them with the key bits once those are in shared memory.
+template <int NSTAGES>
+struct RefRegs {
+  static constexpr int NR = 16 * NSTAGES;
+  static constexpr int kSk = (NR * tdes_gen::kKeyStride + kThreads - 1) / kThreads;
+  static constexpr int kD = (NR * tdes_gen::kDeltaStride + kThreads - 1) / kThreads;
+  static constexpr int kFix = (3 * tdes_gen::kDeltaStride + kThreads - 1) / kThreads;
+  static constexpr int kFin = (64 + kThreads - 1) / kThreads;
+  uint32_t sk[kSk], d[kD], fix[kFix];  // two 16-bit references each
+  uint16_t fin[kFin];
+};
+
+template <int NSTAGES>
+__device__ __forceinline__ void load_refs(RefRegs<NSTAGES>& rr) {
   using namespace tdes_gen;
-  constexpr int NR = 16 * NSTAGES;
+  using RR = RefRegs<NSTAGES>;
   const OpRefs<NSTAGES>& o = refs_dev<NSTAGES>();
-  auto bit = [&](uint16_t ref) -> uint32_t {
+  const uint32_t* sk = reinterpret_cast<const uint32_t*>(&o.sk[0][0][0]);
+  const uint32_t* d = reinterpret_cast<const uint32_t*>(&o.d[0][0][0]);
+  const uint32_t* fix = reinterpret_cast<const uint32_t*>(&o.fix[0][0][0]);
+  const int t = threadIdx.x;
+#pragma unroll
+  for (int j = 0; j < RR::kSk; ++j) {
+    const int i = t + j * kThreads;
+    rr.sk[j] = i < RR::NR * kKeyStride ? sk[i] : 0xFFFFFFFFu;
+  }
+#pragma unroll
+  for (int j = 0; j < RR::kD; ++j) {
+    const int i = t + j * kThreads;
+    rr.d[j] = i < RR::NR * kDeltaStride ? d[i] : 0xFFFFFFFFu;
+  }
+#pragma unroll
+  for (int j = 0; j < RR::kFix; ++j) {
+    const int i = t + j * kThreads;
+    rr.fix[j] = i < 3 * kDeltaStride ? fix[i] : 0xFFFFFFFFu;
+  }
+#pragma unroll
+  for (int j = 0; j < RR::kFin; ++j) {
+    const int i = t + j * kThreads;
+    rr.fin[j] = i < 64 ? o.fin[i] : kNoRef;
+  }
+}
+
+template <int NSTAGES, bool WITH_S>
+__device__ __forceinline__ void expand_keys(const RefRegs<NSTAGES>& rr, const uint64_t* kbits, uint4* smem) {
+  using KT = KeyTable<NSTAGES, WITH_S>;
+  using RR = RefRegs<NSTAGES>;
+  using namespace tdes_gen;
+  auto bit = [&](uint32_t ref) -> uint32_t {
     return ref == kNoRef ? 0u : 0u - (uint32_t)((kbits[ref / 48] >> (47 - ref % 48)) & 1u);
   };
+  auto pair = [&](uint32_t two) { return bit(two & 0xFFFFu) ^ bit(two >> 16); };  // little endian: [0] low
   uint32_t* t32 = reinterpret_cast<uint32_t*>(smem);
-  for (int i = threadIdx.x; i < NR * kKeyStride; i += blockDim.x) {
-    const int r = i / kKeyStride, q = i % kKeyStride;
-    const uint32_t v = bit(o.sk[r][q][0]) ^ bit(o.sk[r][q][1]);
-    if (WITH_S) t32[4 * (r * KT::kSt + KT::kS) + q] = v | 1u;  // s
-    t32[4 * (r * KT::kSt + KT::kK) + q] = v;                   // k
+  const int t = threadIdx.x;
+#pragma unroll
+  for (int j = 0; j < RR::kSk; ++j) {
+    const int i = t + j * kThreads;
+    if (i < RR::NR * kKeyStride) {
+      const int r = i / kKeyStride, q = i % kKeyStride;
+      const uint32_t v = pair(rr.sk[j]);
+      if (WITH_S) t32[4 * (r * KT::kSt + KT::kS) + q] = v | 1u;  // s
+      t32[4 * (r * KT::kSt + KT::kK) + q] = v;                   // k
+    }
   }
-  for (int i = threadIdx.x; i < NR * kDeltaStride; i += blockDim.x) {
-    const int r = i / kDeltaStride, u = i % kDeltaStride;
-    t32[4 * (r * KT::kSt + KT::kD) + u] = bit(o.d[r][u][0]) ^ bit(o.d[r][u][1]);
+#pragma unroll
+  for (int j = 0; j < RR::kD; ++j) {
+    const int i = t + j * kThreads;
+    if (i < RR::NR * kDeltaStride) {
+      const int r = i / kDeltaStride, u = i % kDeltaStride;
+      t32[4 * (r * KT::kSt + KT::kD) + u] = pair(rr.d[j]);
+    }
   }
   uint32_t* ff = t32 + 4 * KT::kTabVecs;
-  for (int i = threadIdx.x; i < 3 * kDeltaStride; i += blockDim.x) {
-    const int b = i / kDeltaStride, t = i % kDeltaStride;
-    const uint32_t v = bit(o.fix[b][t][0]) ^ bit(o.fix[b][t][1]);
-    ff[i] = v | 1u;
-    ff[3 * kDeltaStride + i] = v;
+#pragma unroll
+  for (int j = 0; j < RR::kFix; ++j) {
+    const int i = t + j * kThreads;
+    if (i < 3 * kDeltaStride) {
+      const uint32_t v = pair(rr.fix[j]);
+      ff[i] = v | 1u;
+      ff[3 * kDeltaStride + i] = v;
+    }
   }
-  for (int j = threadIdx.x; j < 64; j += blockDim.x) {
-    const uint32_t v = bit(o.fin[j]);
-    ff[6 * kDeltaStride + j] = v | 1u;
-    ff[6 * kDeltaStride + 64 + j] = v;
+#pragma unroll
+  for (int j = 0; j < RR::kFin; ++j) {
+    const int i = t + j * kThreads;
+    if (i < 64) {
+      const uint32_t v = bit(rr.fin[j]);
+      ff[6 * kDeltaStride + i] = v | 1u;
+      ff[6 * kDeltaStride + 64 + i] = v;
+    }
   }
 }
 
@@ -613,13 +674,16 @@ tdes_ecb_kernel(const uint2* in, uint2* out, size_t nblocks,
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     if (staged) tma_load(buf, in + tile * kTileBlocks, kTileBytes, &tma_bar[warp]);
   }
-  // packed subkeys -> shared memory (warp-uniform parameter loads), then expand
+  // key operands: reference pairs (global) in flight while the packed subkeys go
+  // to shared memory (warp-uniform parameter loads); then expand
+  RefRegs<NSTAGES> rr;
+  load_refs<NSTAGES>(rr);
   for (int r = (int)warp; r < 16 * NSTAGES; r += kWarps) {
     const uint64_t v = kp.k[r];
     if (lane == 0) kbits[r] = v;
   }
   __syncthreads();
-  expand_keys<NSTAGES, DEVKEYS>(kbits, ksm);
+  expand_keys<NSTAGES, DEVKEYS>(rr, kbits, ksm);
   __syncthreads();
   auto claim = [&]() -> size_t {
     unsigned t = 0;

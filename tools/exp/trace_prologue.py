@@ -1,9 +1,9 @@
 """Where a throughput-kernel launch spends its time outside the rounds (experiment).
 
 Builds a copy of the library whose tdes_ecb_kernel records %globaltimer per warp
-(lane 0) at kernel entry, after the prologue's __syncthreads (key table copied,
-mbarriers initialised) and at exit, then (on the GPU) times single launches with
-CUDA events beside the traced span:
+(lane 0) at kernel entry, after its own share of the key expansion, after the
+prologue's final __syncthreads and at exit, then (on the GPU) times single launches
+with CUDA events beside the traced span:
 
   python tools/exp/trace_prologue.py build --out tools/exp/vtrace.so
   TDES_LIB_PATH=tools/exp/vtrace.so python tools/exp/trace_prologue.py run [--mode 1]
@@ -43,12 +43,10 @@ def cmd_build(a):
     entry = "  using KT = KeyTable<NSTAGES, DEVKEYS>;\n"
     assert entry in t
     t = t.replace(entry, entry + "  const unsigned long long t_entry = gtimer();\n", 1)
-    copy = "  extern __shared__ uint4 tma_buf[];  // kTma"
+    copy = "  expand_keys<NSTAGES, DEVKEYS>(rr, kbits, ksm);\n  __syncthreads();\n"
     assert copy in t
-    t = t.replace(copy, "  const unsigned long long t_copy = gtimer();\n" + copy, 1)
-    sync = "  if (kTma) asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");\n  __syncthreads();\n"
-    assert sync in t
-    t = t.replace(sync, sync + "  const unsigned long long t_sync = gtimer();\n", 1)
+    t = t.replace(copy, "  expand_keys<NSTAGES, DEVKEYS>(rr, kbits, ksm);\n  const unsigned long long t_copy = gtimer();\n"
+                  "  __syncthreads();\n  const unsigned long long t_sync = gtimer();\n", 1)
     tail = '''    } else {
       tile = claim();
     }
