@@ -669,14 +669,18 @@ tdes_ecb_kernel(const uint2* in, uint2* out, size_t nblocks,
   if (threadIdx.x == 0) next_tile = kWarps;
   size_t tile = lo + warp;
   bool staged = stageable(tile);
+  // key operands: reference pairs (global) in flight while the packed subkeys go
+  // to shared memory (warp-uniform parameter loads); then expand
+  // (Issuing these loads before the first-tile TMA copies shortens the prologue at
+  // >= 2^24 blocks from ~5 to ~2.2 us -- they no longer queue behind 128 KiB of HBM
+  // reads per SM -- but made whole launches 5-10 us slower (tools/exp/trace_drain.py,
+  // ab_sizes.py), so the TMA copies go first.)
+  RefRegs<NSTAGES> rr;
   if (kTma && lane == 0) {
     mbar_init(&tma_bar[warp]);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     if (staged) tma_load(buf, in + tile * kTileBlocks, kTileBytes, &tma_bar[warp]);
   }
-  // key operands: reference pairs (global) in flight while the packed subkeys go
-  // to shared memory (warp-uniform parameter loads); then expand
-  RefRegs<NSTAGES> rr;
   load_refs<NSTAGES>(rr);
   for (int r = (int)warp; r < 16 * NSTAGES; r += kWarps) {
     const uint64_t v = kp.k[r];
@@ -758,11 +762,17 @@ __device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, unsigned lane) 
 // warps may reach it from the different S-box cases of sbox_by_index.
 __device__ __forceinline__ void team_sync() { asm volatile("bar.sync 0, %0;" ::"n"(kSplitThreads) : "memory"); }
 
-// Per-warp key material for the split kernel: s = k | 1 (+1 / -1) of this warp's
-// S-box's 6 key bits for every round, as 3 x uint2 per round.
+// Per-warp key material for the split kernel: s = k | 1 (+1 / -1) and k (0 / ~0)
+// of this warp's S-box's 6 key bits for every round (48 bytes per round: three
+// LDS.128 and no arithmetic between the load and the round's IMADs, so the loads
+// issued before a barrier complete while the team waits).  Measured against
+// loading s only and rebuilding k = mulhi(c, s) before the barrier: see DESIGN.md §6.
+struct alignas(16) SplitRoundKeys {
+  uint32_t s[6], k[6];
+};
 template <int NROUNDS>
 struct SplitKeys {
-  uint2 s[8][NROUNDS][3];
+  SplitRoundKeys r[8][NROUNDS];
 };
 
 // One round of the split kernel for S-box G: read the E-window of half IN from
@@ -783,16 +793,12 @@ __device__ __forceinline__ void split_round(int G, uint32_t* st, const int (&win
 // Load round r's key operands of this warp (off the critical path: issued before
 // the barrier that ends round r - 1).
 template <int NROUNDS>
-__device__ __forceinline__ void split_keys(const uint2 (&ks)[NROUNDS][3], int r, uint32_t c, uint32_t (&S)[6],
+__device__ __forceinline__ void split_keys(const SplitRoundKeys (&ks)[NROUNDS], int r, uint32_t, uint32_t (&S)[6],
                                            uint32_t (&K)[6]) {
-#pragma unroll
-  for (int j = 0; j < 3; ++j) {
-    const uint2 v = ks[r][j];
-    S[2 * j] = v.x;
-    S[2 * j + 1] = v.y;
-  }
-#pragma unroll
-  for (int i = 0; i < 6; ++i) asm("mul.hi.s32 %0, %1, %2;" : "=r"(K[i]) : "r"(c), "r"(S[i]));  // k = (s - 1) / 2
+  const uint4* v = reinterpret_cast<const uint4*>(&ks[r]);
+  const uint4 a = v[0], b = v[1], d = v[2];
+  S[0] = a.x; S[1] = a.y; S[2] = a.z; S[3] = a.w; S[4] = b.x; S[5] = b.y;
+  K[0] = b.z; K[1] = b.w; K[2] = d.x; K[3] = d.y; K[4] = d.z; K[5] = d.w;
 }
 
 // The whole tile loop for the warp that evaluates S-box G (warp-uniform).  The
@@ -804,7 +810,7 @@ __device__ __forceinline__ void split_keys(const uint2 (&ks)[NROUNDS][3], int r,
 // but slower from 2^17 blocks on (instruction-cache pressure).
 template <int NSTAGES>
 __device__ __forceinline__ void split_body(int G, const uint2* in, uint2* out, size_t nblocks, uint32_t* st,
-                                           const uint2 (&ks)[16 * NSTAGES][3], unsigned lane, uint32_t c) {
+                                           const SplitRoundKeys (&ks)[16 * NSTAGES], unsigned lane, uint32_t c) {
   int win[2][6], own[2][4];
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
@@ -879,23 +885,26 @@ tdes_split_kernel(const uint2* in, uint2* out, size_t nblocks,
   for (int r = lane; r < 16 * NSTAGES; r += 32) {
     const uint32_t kb = (uint32_t)(mk.k[r] >> (42 - 6 * g)) & 63u;
 #pragma unroll
-    for (int j = 0; j < 3; ++j)
-      ks.s[g][r][j] = make_uint2(1u - (((kb >> (5 - 2 * j)) & 1u) << 1), 1u - (((kb >> (4 - 2 * j)) & 1u) << 1));
+    for (int i = 0; i < 6; ++i) {
+      const uint32_t k = 0u - ((kb >> (5 - i)) & 1u);
+      ks.r[g][r].s[i] = k | 1u;
+      ks.r[g][r].k[i] = k;
+    }
   }
   __syncwarp();
   if (SPEC) {
     switch (g) {  // a constant S-box index per case: split_body is inlined and specialised
-      case 0: split_body<NSTAGES>(0, in, out, nblocks, st, ks.s[0], lane, c); break;
-      case 1: split_body<NSTAGES>(1, in, out, nblocks, st, ks.s[1], lane, c); break;
-      case 2: split_body<NSTAGES>(2, in, out, nblocks, st, ks.s[2], lane, c); break;
-      case 3: split_body<NSTAGES>(3, in, out, nblocks, st, ks.s[3], lane, c); break;
-      case 4: split_body<NSTAGES>(4, in, out, nblocks, st, ks.s[4], lane, c); break;
-      case 5: split_body<NSTAGES>(5, in, out, nblocks, st, ks.s[5], lane, c); break;
-      case 6: split_body<NSTAGES>(6, in, out, nblocks, st, ks.s[6], lane, c); break;
-      default: split_body<NSTAGES>(7, in, out, nblocks, st, ks.s[7], lane, c); break;
+      case 0: split_body<NSTAGES>(0, in, out, nblocks, st, ks.r[0], lane, c); break;
+      case 1: split_body<NSTAGES>(1, in, out, nblocks, st, ks.r[1], lane, c); break;
+      case 2: split_body<NSTAGES>(2, in, out, nblocks, st, ks.r[2], lane, c); break;
+      case 3: split_body<NSTAGES>(3, in, out, nblocks, st, ks.r[3], lane, c); break;
+      case 4: split_body<NSTAGES>(4, in, out, nblocks, st, ks.r[4], lane, c); break;
+      case 5: split_body<NSTAGES>(5, in, out, nblocks, st, ks.r[5], lane, c); break;
+      case 6: split_body<NSTAGES>(6, in, out, nblocks, st, ks.r[6], lane, c); break;
+      default: split_body<NSTAGES>(7, in, out, nblocks, st, ks.r[7], lane, c); break;
     }
   } else {
-    split_body<NSTAGES>(g, in, out, nblocks, st, ks.s[g], lane, c);
+    split_body<NSTAGES>(g, in, out, nblocks, st, ks.r[g], lane, c);
   }
 }
 
