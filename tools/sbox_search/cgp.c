@@ -29,7 +29,9 @@
  *   depth_mode = 4: sample -- neutral drift among exact circuits of at most the
  *   starting gate count, printing the current circuit every 2^L generations
  *   (L = argv[6], default 22; smaller L = variants closer to the start)
- *   (structurally different equal-cost alternatives, for measured selection).
+ *   (structurally different equal-cost alternatives, for measured selection);
+ *   argv[7] (default 0) lets the drift use that many gates more than the start
+ *   (tools/run_resub.py then resubstitutes each sample).
  *   depth_mode = 3: polish -- minimise (gates, -foldable outputs, depth) (a folded
  *   output saves the round one key IMAD; measured worth about half a gate).
  *   depth_mode = 1: minimise (gates, depth) lexicographically -- a child is accepted
@@ -319,7 +321,7 @@ int main(int argc, char **argv) {
     return 0;
   }
   if (depth_mode == 4) {
-    const int cap = pc;
+    const int cap = pc + (argc > 7 ? atoi(argv[7]) : 0);  /* argv[7]: drift up to this many gates more */
     const long every = (1L << (argc > 6 ? atoi(argv[6]) : 22)) - 1;
     for (;;) {
       if ((++gen & 0xFFFF) == 0 && (double)(clock() - t0) / CLOCKS_PER_SEC > secs) break;
