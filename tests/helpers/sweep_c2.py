@@ -67,14 +67,15 @@ def check(keys, x, y, decrypt, n):
     return np.array_equal(got, exp), len(idx)
 
 
-def oracle_time(keys, n, cap_s, rate):
-    """Full-size oracle wall time if it fits the cap, else a timed sample scaled up."""
+def oracle_time(keys, n, cap_s, rate, threads=0):
+    """Full-size oracle wall time if it fits the cap, else a timed sample scaled up
+    (threads <= 0: all OpenMP threads; SURVEY 8(d) asks for 1 thread and all)."""
     est = n / rate if rate else 0
-    m = n if est <= cap_s else max(1 << 16, int(cap_s * rate) // 4)
+    m = n if est <= cap_s else max(1 << 14, int(cap_s * rate) // 4)
     p = synthetic.plaintext_bytes(0, m)
     out = np.empty_like(p)
     t0 = time.perf_counter()
-    oracle.tdes_ecb_into(*keys, p, out)
+    oracle.tdes_ecb_into(*keys, p, out, threads=threads)
     dt = time.perf_counter() - t0
     return dt * n / m, m == n, m / dt
 
@@ -89,16 +90,17 @@ def main():
     tdes.fill_splitmix64(x)
     y = torch.empty_like(x)
     cores = len(os.sched_getaffinity(0))
-    rate = None
+    rate = rate1 = None
     lines = ["# Config 2: size sweep, 3DES-EDE ECB on one B200 vs the oracle on host cores", "",
              f"GPU: {torch.cuda.get_device_name(0)}; host cores used by the oracle: {cores} (OpenMP over blocks).",
              "Device time = one launch queued behind a device-side sleep (median of 10, CUDA events, data",
              "resident in HBM): the launch's own device time, no host submission latency.  Beside it: the",
              "same launch on an idle GPU (adds the host's submission latency) and 20 launches back to back.",
              "Oracle = `oracle/tdes_oracle.c` (char per bit, as in the paper), wall clock;",
-             "`~` = extrapolated from a timed sample (the full size would exceed the per-point cap).", "",
-             "| blocks | bytes | op | keys | GPU ms | GPU GB/s | idle-launch GB/s | back-to-back GB/s | bit-exact (blocks checked) | oracle s | oracle GB/s | GPU/oracle |",
-             "|---|---|---|---|---|---|---|---|---|---|---|---|"]
+             "`~` = extrapolated from a timed sample (the full size would exceed the per-point cap).",
+             "The oracle is timed on all host threads and on 1 thread (SURVEY 8(d)).", "",
+             "| blocks | bytes | op | keys | GPU ms | GPU GB/s | idle-launch GB/s | back-to-back GB/s | bit-exact (blocks checked) | oracle s | oracle GB/s | GPU/oracle | oracle 1-thread s | GPU/oracle 1-thread |",
+             "|---|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
     points = [(e, op, "3-key") for e in range(17, 28) for op in ("enc", "dec")]
     points += [(25, op, k) for k in ("1-key", "2-key") for op in ("enc", "dec")]
     keysets = {"3-key": synthetic.KEYS_3KEY, "2-key": synthetic.KEYS_2KEY, "1-key": synthetic.KEYS_1KEY}
@@ -113,12 +115,14 @@ def main():
         ok, nchk = check(keys, xs, ys, dec, n)
         osec, full, r = oracle_time(keys, n, a.cap, rate)
         rate = rate or r
+        osec1, full1, r1 = oracle_time(keys, n, a.cap / 4, rate1, threads=1)
+        rate1 = rate1 or r1
         gbs = n * 8 / ms / 1e6
         ogbs = n * 8 / osec / 1e9
         lines.append(f"| 2^{e} | {n * 8 / 2**20:g} MiB | {op} | {kname} | {ms:.4f} | {gbs:.1f} | "
                      f"{n * 8 / ms_idle / 1e6:.1f} | {n * 8 / ms_b2b / 1e6:.1f} | "
                      f"{'yes' if ok else 'NO'} ({nchk}) | {'' if full else '~'}{osec:.2f} | {ogbs:.4f} | "
-                     f"{gbs / ogbs:.0f}x |")
+                     f"{gbs / ogbs:.0f}x | {'' if full1 else '~'}{osec1:.2f} | {gbs / (n * 8 / osec1 / 1e9):.0f}x |")
         print(lines[-1], flush=True)
     os.makedirs(os.path.dirname(a.out) or ".", exist_ok=True)
     with open(a.out, "w") as f:

@@ -34,7 +34,12 @@ import run_cgp  # noqa: E402
 SEL = os.path.join(HERE, "sel")
 
 
-def samples(g, circ, secs, seed, log_every=22):
+def folds(c):
+    n = gen_tdes.normalize_outputs(c)
+    return sum(1 for o, f in enumerate(n.get("fuse") or [None] * 4) if f is None or o in gen_tdes.fold_producers(n))
+
+
+def samples(g, circ, secs, seed, log_every=22, keep_folds=False):
     p = subprocess.run([run_cgp.BIN, str(secs), str(seed), "4", "4", "4", str(log_every)],
                        input=run_cgp.to_stdin(g, circ),
                        capture_output=True, text=True)
@@ -45,6 +50,8 @@ def samples(g, circ, secs, seed, log_every=22):
         c["fuse"] = [None if f is None else list(f) for f in c["fuse"]]
         key = json.dumps(c["gates"])
         if key in seen or not gen_tdes.verify_circuit(g, c):
+            continue
+        if keep_folds and folds(c) < folds(circ):  # a lost fold costs a key IMAD per round
             continue
         seen.add(key)
         out.append(c)
@@ -67,7 +74,7 @@ def cmd_build(a):
     cur = gen_tdes.choose_circuits()
     boxes = [int(b) - 1 for b in a.boxes.split(",")]
     with ThreadPoolExecutor(len(boxes)) as ex:
-        got = dict(zip(boxes, ex.map(lambda g: samples(g, cur[g], a.seconds, a.seed + g, a.log_every), boxes)))
+        got = dict(zip(boxes, ex.map(lambda g: samples(g, cur[g], a.seconds, a.seed + g, a.log_every, a.keep_folds), boxes)))
     tmp = tempfile.mkdtemp(prefix="sel_")
     jobs = [(os.path.join(SEL, "base.so"), base_files, "")]
     manifest = {}
@@ -132,6 +139,7 @@ def main():
     b.add_argument("--jobs", type=int, default=8)
     b.add_argument("--seed", type=int, default=1000)
     b.add_argument("--log-every", type=int, default=22, help="sample every 2^L generations (smaller: nearer variants)")
+    b.add_argument("--keep-folds", action="store_true", help="only samples with at least the start's foldable outputs")
     p = sub.add_parser("pick")
     p.add_argument("results")
     p.add_argument("--min-gain", type=float, default=0.3)

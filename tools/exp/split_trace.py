@@ -1,4 +1,8 @@
-"""Per-round clock64 timeline of the split kernel (experiment aid; needs tools/exp/strace.so)."""
+"""Per-round clock64 timeline of the split kernel (experiment aid).
+
+  python tools/exp/split_trace_build.py   # -> tools/exp/strace.so
+  TDES_LIB_PATH=tools/exp/strace.so python tools/exp/split_trace.py [nblocks ...]
+"""
 import ctypes
 import os
 import sys
@@ -9,7 +13,8 @@ import paper_2007_10752_b200 as tdes  # noqa: E402
 import synthetic  # noqa: E402
 
 s = tdes.key_schedule(*synthetic.KEYS_3KEY)
-for n in (1024, 1 << 17):
+tdes._lib.tdes_get_strace.argtypes = [ctypes.c_void_p]
+for n in [int(a) for a in sys.argv[1:]] or (1024, 1 << 17):
     x = torch.empty(8 * n, dtype=torch.uint8, device="cuda"); tdes.fill_splitmix64(x)
     y = torch.empty_like(x)
     for _ in range(3):
