@@ -801,16 +801,16 @@ __device__ __forceinline__ void split_keys(const SplitRoundKeys (&ks)[NROUNDS], 
   K[0] = b.z; K[1] = b.w; K[2] = d.x; K[3] = d.y; K[4] = d.z; K[5] = d.w;
 }
 
-// The whole tile loop for the warp that evaluates S-box G (warp-uniform).  The
-// rounds run in (A, B) / (B, A) pairs, so no per-round branch picks the half;
-// the key operands of the next round are loaded before each barrier.  Measured
-// (B200, back-to-back 3DES launches): 16.5 -> 14.4 us for 1-16 tiles, 16.5 -> 14.5
-// us at 2^17 blocks, 20.5 -> 18.5 us at 2^18.  A compile-time S-box index per
-// warp (eight specialised copies of the loop) was faster for 1-16 tiles (12.5 us)
-// but slower from 2^17 blocks on (instruction-cache pressure).
-template <int NSTAGES>
-__device__ __forceinline__ void split_body(int G, const uint2* in, uint2* out, size_t nblocks, uint32_t* st,
-                                           const SplitRoundKeys (&ks)[16 * NSTAGES], unsigned lane, uint32_t c) {
+// The 48 rounds of one tile for the warp that evaluates S-box G (warp-uniform;
+// GC >= 0: G = GC known at compile time, the S-box-specialised variant).  The
+// rounds run in (A, B) / (B, A) pairs, so no per-round branch picks the half; the
+// key operands of the next round are loaded before each barrier.  Measured (B200,
+// back-to-back 3DES launches): 16.5 -> 14.4 us for 1-16 tiles, 16.5 -> 14.5 us at
+// 2^17 blocks, 20.5 -> 18.5 us at 2^18.
+template <int NSTAGES, int GC>
+__device__ __forceinline__ void split_rounds(int G_, uint32_t* st, const SplitRoundKeys (&ks)[16 * NSTAGES],
+                                             unsigned lane, uint32_t c) {
+  const int G = GC >= 0 ? GC : G_;
   int win[2][6], own[2][4];
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
@@ -819,6 +819,43 @@ __device__ __forceinline__ void split_body(int G, const uint2* in, uint2* out, s
 #pragma unroll
     for (int o = 0; o < 4; ++o) own[h][o] = tdes_gen::kOwn[h][G][o] * kStride + lane;
   }
+  uint32_t S[6], K[6];
+  split_keys(ks, 0, c, S, K);
+  team_sync();
+  uint32_t H[2][4];  // the planes of half A (0) and B (1) this warp's S-box writes
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int o = 0; o < 4; ++o) H[h][o] = st[own[h][o]];
+  // stage s round rr updates A iff (rr + s) is even: stages 0 and 2
+  // run (A, B) pairs, stage 1 (B, A) pairs.  Updating A reads half B (IN = 1).
+#pragma unroll
+  for (int stage = 0; stage < NSTAGES; ++stage) {
+#pragma unroll 1
+    for (int rr = 0; rr < 16; rr += 2) {
+      const int r = 16 * stage + rr;
+      if (stage & 1) split_round<0>(G, st, win, own, H, S, K);
+      else split_round<1>(G, st, win, own, H, S, K);
+      split_keys(ks, r + 1, c, S, K);
+      team_sync();
+      if (stage & 1) split_round<1>(G, st, win, own, H, S, K);
+      else split_round<0>(G, st, win, own, H, S, K);
+      if (r + 2 < 16 * NSTAGES) split_keys(ks, r + 2, c, S, K);
+      team_sync();
+    }
+  }
+}
+
+// The tile loop of warp G: load (lane-parallel transposes into the shared round
+// state), the rounds, store.  SPEC: the rounds run in a copy specialised for the
+// warp's S-box (no per-round dispatch).  Only the rounds are specialised: the load
+// and store stay outside the per-S-box switch, where the compiler knows the warp
+// is converged (inside it, every warp shuffle got a divergence fallback and the
+// specialised kernel grew to 220 KB of code, slower than the dispatching one from
+// 2^17 blocks on).
+template <int NSTAGES, bool SPEC>
+__device__ __forceinline__ void split_body(int G, const uint2* in, uint2* out, size_t nblocks, uint32_t* st,
+                                           const SplitRoundKeys (&ks)[16 * NSTAGES], unsigned lane, uint32_t c) {
   const size_t ntiles = (nblocks + kGroupBlocks - 1) / kGroupBlocks;
   for (size_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const size_t base = tile * kGroupBlocks;
@@ -831,30 +868,20 @@ __device__ __forceinline__ void split_body(int G, const uint2* in, uint2* out, s
       st[lane * kStride + q] = warp_transpose32(v.x, lane);  // plane `lane` of group q
       st[(32 + lane) * kStride + q] = warp_transpose32(v.y, lane);
     }
-    uint32_t S[6], K[6];
-    split_keys(ks, 0, c, S, K);
-    team_sync();
-    uint32_t H[2][4];  // the planes of half A (0) and B (1) this warp's S-box writes
-#pragma unroll
-    for (int h = 0; h < 2; ++h)
-#pragma unroll
-      for (int o = 0; o < 4; ++o) H[h][o] = st[own[h][o]];
-    // stage s round rr updates A iff (rr + s) is even: stages 0 and 2
-    // run (A, B) pairs, stage 1 (B, A) pairs.  Updating A reads half B (IN = 1).
-#pragma unroll
-    for (int stage = 0; stage < NSTAGES; ++stage) {
-#pragma unroll 1
-      for (int rr = 0; rr < 16; rr += 2) {
-        const int r = 16 * stage + rr;
-        if (stage & 1) split_round<0>(G, st, win, own, H, S, K);
-        else split_round<1>(G, st, win, own, H, S, K);
-        split_keys(ks, r + 1, c, S, K);
-        team_sync();
-        if (stage & 1) split_round<1>(G, st, win, own, H, S, K);
-        else split_round<0>(G, st, win, own, H, S, K);
-        if (r + 2 < 16 * NSTAGES) split_keys(ks, r + 2, c, S, K);
-        team_sync();
+    if (SPEC) {
+      switch (G) {  // a constant S-box index per case: split_rounds is inlined and specialised
+        case 0: split_rounds<NSTAGES, 0>(G, st, ks, lane, c); break;
+        case 1: split_rounds<NSTAGES, 1>(G, st, ks, lane, c); break;
+        case 2: split_rounds<NSTAGES, 2>(G, st, ks, lane, c); break;
+        case 3: split_rounds<NSTAGES, 3>(G, st, ks, lane, c); break;
+        case 4: split_rounds<NSTAGES, 4>(G, st, ks, lane, c); break;
+        case 5: split_rounds<NSTAGES, 5>(G, st, ks, lane, c); break;
+        case 6: split_rounds<NSTAGES, 6>(G, st, ks, lane, c); break;
+        default: split_rounds<NSTAGES, 7>(G, st, ks, lane, c); break;
       }
+      __syncwarp();  // converged again (keeps the store's shuffles free of divergence fallbacks)
+    } else {
+      split_rounds<NSTAGES, -1>(G, st, ks, lane, c);
     }
     // FP (renaming) + store: warp G writes groups 4G..4G+3
 #pragma unroll
@@ -869,10 +896,12 @@ __device__ __forceinline__ void split_body(int G, const uint2* in, uint2* out, s
   }
 }
 
-// SPEC: every warp runs a copy of the loop specialised for its S-box (no per-round
-// dispatch; 8x the code).  Measured (B200, back-to-back launches): 1 tile 14.4 ->
-// 12.5 us, 16 tiles 14.4 -> 13.7 us, but 128 tiles 14.5 -> 16.4 us (instruction
-// fetch), so launches of at most kSplitSpecMaxTiles tiles use it.
+// SPEC: every warp runs the rounds in a copy specialised for its S-box (no per-round
+// dispatch).  With the load and store outside the per-S-box switch (split_body) the
+// kernel is 3.2 K instructions (51 KB) instead of 13.8 K, and it is faster at every
+// split size: 128 tiles (C1) 14.2 -> 12.3 us back to back, 27.8 -> 23.4 us single
+// (profiles/r02/split_spec_ab.txt), so auto mode always uses it; the dispatching
+// variant stays as a -DTDES_SPLIT_SPEC_MAX=<tiles> experiment switch.
 template <int NSTAGES, bool SPEC>
 __global__ void __launch_bounds__(kSplitThreads)
 tdes_split_kernel(const uint2* in, uint2* out, size_t nblocks,
@@ -892,20 +921,7 @@ tdes_split_kernel(const uint2* in, uint2* out, size_t nblocks,
     }
   }
   __syncwarp();
-  if (SPEC) {
-    switch (g) {  // a constant S-box index per case: split_body is inlined and specialised
-      case 0: split_body<NSTAGES>(0, in, out, nblocks, st, ks.r[0], lane, c); break;
-      case 1: split_body<NSTAGES>(1, in, out, nblocks, st, ks.r[1], lane, c); break;
-      case 2: split_body<NSTAGES>(2, in, out, nblocks, st, ks.r[2], lane, c); break;
-      case 3: split_body<NSTAGES>(3, in, out, nblocks, st, ks.r[3], lane, c); break;
-      case 4: split_body<NSTAGES>(4, in, out, nblocks, st, ks.r[4], lane, c); break;
-      case 5: split_body<NSTAGES>(5, in, out, nblocks, st, ks.r[5], lane, c); break;
-      case 6: split_body<NSTAGES>(6, in, out, nblocks, st, ks.r[6], lane, c); break;
-      default: split_body<NSTAGES>(7, in, out, nblocks, st, ks.r[7], lane, c); break;
-    }
-  } else {
-    split_body<NSTAGES>(g, in, out, nblocks, st, ks.r[g], lane, c);
-  }
+  split_body<NSTAGES, SPEC>(g, in, out, nblocks, st, ks.r[g], lane, c);
 }
 
 // ------------------------------------------------------------ launching ---
@@ -960,7 +976,10 @@ int check_buffers(const void* in, const void* out, size_t nblocks) {
 // Auto mode: the split (latency) kernel for launches of at most this many
 // 1024-block tiles, the throughput kernel above (measured crossover).
 constexpr size_t kSplitMaxTiles = 296;
-constexpr size_t kSplitSpecMaxTiles = 16;  // the S-box-specialised split kernel (tdes_split_kernel<., true>)
+#ifndef TDES_SPLIT_SPEC_MAX
+#define TDES_SPLIT_SPEC_MAX 296
+#endif
+constexpr size_t kSplitSpecMaxTiles = TDES_SPLIT_SPEC_MAX;  // the S-box-specialised split kernel (tdes_split_kernel<., true>)
 // Auto mode uses the throughput kernel whose s operands stay in the launch
 // parameters (mode 1) above kSplitMaxTiles.  (Until its prologue expanded k and d
 // on the device and issued the first tile's TMA copy before that expansion, the
