@@ -143,6 +143,26 @@ def subkeys(s: TdesSchedule) -> list[list[int]]:
     return [[int(s.subkey[k][r]) for r in range(16)] for k in range(3)]
 
 
+# Per-call host cost matters for small launches (a C1 launch is ~12 us of device
+# time): the public torch.cuda.current_stream() and torch.cuda.device() cost ~2.2 and
+# ~1.5 us per call (tools/exp/binding_overhead.py), so the binding uses torch's raw
+# accessors when they exist and enters the device context only when the tensor is
+# not on the current device.
+_RAW_STREAM = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+_GET_DEVICE = getattr(torch._C, "_cuda_getDevice", None)
+
+
+def _launch(device: torch.device, call, stream):
+    """Run ``call(stream_handle)`` with ``device`` current (the C ABI launches on the
+    current device) on ``stream`` (default: that device's current stream)."""
+    idx = device.index
+    h = _RAW_STREAM(idx) if stream is None and _RAW_STREAM is not None else _stream_handle(stream, device)
+    if _GET_DEVICE is not None and _GET_DEVICE() == idx:
+        return call(h)
+    with torch.cuda.device(device):
+        return call(h)
+
+
 def _stream_handle(stream, device=None) -> int:
     """The raw handle of `stream` (default: the current stream of `device`).
 
@@ -171,9 +191,8 @@ def _prep(x: torch.Tensor, out):
 
 def _crypt(fn, sched, x, out, stream, what):
     out = _prep(x, out)
-    with torch.cuda.device(x.device):
-        _check(fn(ctypes.byref(sched), x.data_ptr(), out.data_ptr(), x.numel() // 8,
-                  _stream_handle(stream, x.device)), what)
+    _check(_launch(x.device, lambda h: fn(ctypes.byref(sched), x.data_ptr(), out.data_ptr(), x.numel() // 8, h),
+                   stream), what)
     return out
 
 
@@ -198,10 +217,9 @@ def des_ecb_decrypt(x, sched: DesSchedule, out=None, stream=None):
 def ecb_crypt_mode(x: torch.Tensor, sched: TdesSchedule, mode: int, decrypt=False, out=None, stream=None):
     """3DES ECB with an explicit kernel choice (MODE_AUTO / MODE_THROUGHPUT / MODE_SPLIT / MODE_DEVKEYS)."""
     out = _prep(x, out)
-    with torch.cuda.device(x.device):
-        _check(_lib.tdes_ecb_crypt_mode(ctypes.byref(sched), int(bool(decrypt)), x.data_ptr(), out.data_ptr(),
-                                        x.numel() // 8, mode, _stream_handle(stream, x.device)),
-               "tdes_ecb_crypt_mode")
+    _check(_launch(x.device, lambda h: _lib.tdes_ecb_crypt_mode(ctypes.byref(sched), int(bool(decrypt)), x.data_ptr(),
+                                                               out.data_ptr(), x.numel() // 8, mode, h), stream),
+           "tdes_ecb_crypt_mode")
     return out
 
 

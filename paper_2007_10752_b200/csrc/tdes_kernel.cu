@@ -1059,6 +1059,26 @@ const SKeys<16 * NSTAGES>& cached_skeys(const uint32_t (*masks)[48]) {
   return e.sk;
 }
 
+// The packed subkeys (the split kernel's and mode 3's launch parameter), cached the
+// same way: packing costs ~2 us of host time per call, a hit one 9 KB memcmp.
+template <int NSTAGES>
+const RoundKeys<16 * NSTAGES>& cached_rkeys(const uint32_t (*masks)[48]) {
+  struct Entry {
+    uint32_t key[16 * NSTAGES][48];
+    RoundKeys<16 * NSTAGES> rk;
+    bool valid = false;
+  };
+  thread_local Entry cache[2];
+  thread_local int next = 0;
+  for (Entry& e : cache)
+    if (e.valid && memcmp(e.key, masks, sizeof e.key) == 0) return e.rk;
+  Entry& e = cache[next];
+  next ^= 1;
+  memcpy(e.key, masks, sizeof e.key);
+  e.rk = pack_keys<NSTAGES>(masks);
+  e.valid = true;
+  return e.rk;
+}
 
 template <int NSTAGES, bool DEVKEYS>
 cudaError_t launch_throughput(const KeyParam<NSTAGES, DEVKEYS>& kp, const uint2* pin, uint2* pout, size_t nblocks,
@@ -1095,7 +1115,7 @@ int launch(const uint32_t (*masks)[48], const void* in, void* out, size_t nblock
   if (mode == 2 || (mode == 0 && ngroups <= kSplitMaxTiles)) {
     const size_t cap = (size_t)num_sms(dev) * 8u;  // up to 8 teams per SM
     const unsigned sgrid = (unsigned)(ngroups < cap ? ngroups : cap);
-    const RoundKeys<16 * NSTAGES> ms = pack_keys<NSTAGES>(masks);
+    const RoundKeys<16 * NSTAGES>& ms = cached_rkeys<NSTAGES>(masks);
     if (ngroups <= kSplitSpecMaxTiles)
       tdes_split_kernel<NSTAGES, true><<<sgrid, kSplitThreads, 0, stream>>>(
           static_cast<const uint2*>(in), static_cast<uint2*>(out), nblocks, ms, kMulhiC);
@@ -1108,7 +1128,7 @@ int launch(const uint32_t (*masks)[48], const void* in, void* out, size_t nblock
   const uint2* pin = static_cast<const uint2*>(in);
   uint2* pout = static_cast<uint2*>(out);
   if (mode == 3)
-    e = launch_throughput<NSTAGES, true>(pack_keys<NSTAGES>(masks), pin, pout, nblocks, vec4, dev, stream);
+    e = launch_throughput<NSTAGES, true>(cached_rkeys<NSTAGES>(masks), pin, pout, nblocks, vec4, dev, stream);
   else
     e = launch_throughput<NSTAGES, false>(cached_skeys<NSTAGES>(masks), pin, pout, nblocks, vec4, dev, stream);
   if (e != cudaSuccess) return cuda_fail(e);
