@@ -20,8 +20,11 @@
  *     blocks").  Lengths are counts of blocks (size_t, 64-bit indexing).
  *   - Return values: 0 = TDES_OK, otherwise a negative TDES_ERR_* code.  No C++
  *     exception crosses this boundary.  All functions are thread-safe and
- *     re-entrant; the library keeps no mutable global state apart from a
- *     read-only per-device launch-geometry cache.
+ *     re-entrant; the library keeps no shared mutable state apart from a
+ *     per-device launch-geometry cache (written once per device, atomically),
+ *     and each host thread caches the launch operands of the last two key
+ *     schedules it used (thread-local, keyed by the schedule's contents, so a
+ *     caller may reuse or modify a tdes_schedule freely).
  */
 #ifndef TDES_H_
 #define TDES_H_
