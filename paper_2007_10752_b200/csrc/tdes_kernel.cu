@@ -734,8 +734,13 @@ tdes_ecb_kernel(const uint2* in, uint2* out, size_t nblocks,
 // patterns are bank-conflict free); every thread keeps the 4 planes of each
 // half that its S-box writes (P is a permutation, so these partition each
 // half) in registers and publishes them after each update; one barrier per
-// round.  Transposes are lane-parallel (5 shuffle butterfly stages).
-constexpr int kSplitThreads = 256;   // one team = 8 warps
+// round.  Transposes are lane-parallel (5 shuffle butterfly stages).  From 149
+// tiles on (more than one team per SM) teams of 4 warps run two adjacent S-boxes
+// per warp (SPW = 2): two independent S-box chains per warp, one warp per SMSP.
+// SPW = S-boxes per warp: 1 = a team of 8 warps (one S-box each), 2 = a team of
+// 4 warps (two adjacent S-boxes each); the launcher picks by size.
+template <int SPW>
+constexpr int kSplitThreads = 256 / SPW;  // one team
 constexpr int kStride = 33;
 
 // 32x32 bit transpose across a warp: lane i holds row i on entry; on exit lane
@@ -760,45 +765,62 @@ __device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, unsigned lane) 
 
 // Team barrier.  bar.sync counts arriving threads per barrier id, so the eight
 // warps may reach it from the different S-box cases of sbox_by_index.
-__device__ __forceinline__ void team_sync() { asm volatile("bar.sync 0, %0;" ::"n"(kSplitThreads) : "memory"); }
+template <int SPW>
+__device__ __forceinline__ void team_sync() {
+  asm volatile("bar.sync 0, %0;" ::"n"(kSplitThreads<SPW>) : "memory");
+}
 
 // Per-warp key material for the split kernel: s = k | 1 (+1 / -1) and k (0 / ~0)
 // of this warp's S-box's 6 key bits for every round (48 bytes per round: three
 // LDS.128 and no arithmetic between the load and the round's IMADs, so the loads
 // issued before a barrier complete while the team waits).  Measured against
 // loading s only and rebuilding k = mulhi(c, s) before the barrier: see DESIGN.md §6.
+template <int SPW>
 struct alignas(16) SplitRoundKeys {
-  uint32_t s[6], k[6];
+  uint32_t s[6 * SPW], k[6 * SPW];
 };
-template <int NROUNDS>
+template <int SPW, int NROUNDS>
 struct SplitKeys {
-  SplitRoundKeys r[8][NROUNDS];
+  SplitRoundKeys<SPW> r[8 / SPW][NROUNDS];
 };
 
 // One round of the split kernel for S-box G: read the E-window of half IN from
 // shared memory, key XOR (s, k prefetched a round earlier), S-box, publish the 4
 // planes of the other half this warp owns.
-template <int IN>
-__device__ __forceinline__ void split_round(int G, uint32_t* st, const int (&win)[2][6], const int (&own)[2][4],
-                                            uint32_t (&H)[2][4], const uint32_t (&S)[6], const uint32_t (&K)[6]) {
+template <int SPW, int IN>
+__device__ __forceinline__ void split_round(int G, uint32_t* st, const int (&win)[2][6 * SPW],
+                                            const int (&own)[2][4 * SPW], uint32_t (&H)[2][4 * SPW],
+                                            const uint32_t (&S)[6 * SPW], const uint32_t (&K)[6 * SPW]) {
   constexpr int OUT = 1 - IN;
-  uint32_t x[6];
 #pragma unroll
-  for (int i = 0; i < 6; ++i) x[i] = tdes_gen::kxor<false>(st[win[IN][i]], S[i], K[i], 0u);
-  tdes_gen::sbox_by_index(G, x[0], x[1], x[2], x[3], x[4], x[5], H[OUT][0], H[OUT][1], H[OUT][2], H[OUT][3]);
+  for (int j = 0; j < SPW; ++j) {
+    uint32_t x[6];
 #pragma unroll
-  for (int o = 0; o < 4; ++o) st[own[OUT][o]] = H[OUT][o];
+    for (int i = 0; i < 6; ++i) x[i] = tdes_gen::kxor<false>(st[win[IN][6 * j + i]], S[6 * j + i], K[6 * j + i], 0u);
+    tdes_gen::sbox_by_index(SPW * G + j, x[0], x[1], x[2], x[3], x[4], x[5], H[OUT][4 * j], H[OUT][4 * j + 1],
+                            H[OUT][4 * j + 2], H[OUT][4 * j + 3]);
+  }
+#pragma unroll
+  for (int o = 0; o < 4 * SPW; ++o) st[own[OUT][o]] = H[OUT][o];
 }
 
 // Load round r's key operands of this warp (off the critical path: issued before
 // the barrier that ends round r - 1).
-template <int NROUNDS>
-__device__ __forceinline__ void split_keys(const SplitRoundKeys (&ks)[NROUNDS], int r, uint32_t, uint32_t (&S)[6],
-                                           uint32_t (&K)[6]) {
+template <int SPW, int NROUNDS>
+__device__ __forceinline__ void split_keys(const SplitRoundKeys<SPW> (&ks)[NROUNDS], int r, uint32_t,
+                                           uint32_t (&S)[6 * SPW], uint32_t (&K)[6 * SPW]) {
   const uint4* v = reinterpret_cast<const uint4*>(&ks[r]);
-  const uint4 a = v[0], b = v[1], d = v[2];
-  S[0] = a.x; S[1] = a.y; S[2] = a.z; S[3] = a.w; S[4] = b.x; S[5] = b.y;
-  K[0] = b.z; K[1] = b.w; K[2] = d.x; K[3] = d.y; K[4] = d.z; K[5] = d.w;
+  uint32_t w[12 * SPW];
+#pragma unroll
+  for (int q = 0; q < 3 * SPW; ++q) {
+    const uint4 a = v[q];
+    w[4 * q] = a.x; w[4 * q + 1] = a.y; w[4 * q + 2] = a.z; w[4 * q + 3] = a.w;
+  }
+#pragma unroll
+  for (int i = 0; i < 6 * SPW; ++i) {
+    S[i] = w[i];
+    K[i] = w[6 * SPW + i];
+  }
 }
 
 // The 48 rounds of one tile for the warp that evaluates S-box G (warp-uniform;
@@ -807,26 +829,29 @@ __device__ __forceinline__ void split_keys(const SplitRoundKeys (&ks)[NROUNDS], 
 // key operands of the next round are loaded before each barrier.  Measured (B200,
 // back-to-back 3DES launches): 16.5 -> 14.4 us for 1-16 tiles, 16.5 -> 14.5 us at
 // 2^17 blocks, 20.5 -> 18.5 us at 2^18.
-template <int NSTAGES, int GC>
-__device__ __forceinline__ void split_rounds(int G_, uint32_t* st, const SplitRoundKeys (&ks)[16 * NSTAGES],
+template <int SPW, int NSTAGES, int GC>
+__device__ __forceinline__ void split_rounds(int G_, uint32_t* st, const SplitRoundKeys<SPW> (&ks)[16 * NSTAGES],
                                              unsigned lane, uint32_t c) {
-  const int G = GC >= 0 ? GC : G_;
-  int win[2][6], own[2][4];
+  const int G = GC >= 0 ? GC : G_;   // this warp: S-boxes SPW*G .. SPW*G + SPW - 1
+  int win[2][6 * SPW], own[2][4 * SPW];
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
 #pragma unroll
-    for (int i = 0; i < 6; ++i) win[h][i] = tdes_gen::kWin[h][G][i] * kStride + lane;
+    for (int j = 0; j < SPW; ++j) {
 #pragma unroll
-    for (int o = 0; o < 4; ++o) own[h][o] = tdes_gen::kOwn[h][G][o] * kStride + lane;
+      for (int i = 0; i < 6; ++i) win[h][6 * j + i] = tdes_gen::kWin[h][SPW * G + j][i] * kStride + lane;
+#pragma unroll
+      for (int o = 0; o < 4; ++o) own[h][4 * j + o] = tdes_gen::kOwn[h][SPW * G + j][o] * kStride + lane;
+    }
   }
-  uint32_t S[6], K[6];
+  uint32_t S[6 * SPW], K[6 * SPW];
   split_keys(ks, 0, c, S, K);
-  team_sync();
-  uint32_t H[2][4];  // the planes of half A (0) and B (1) this warp's S-box writes
+  team_sync<SPW>();
+  uint32_t H[2][4 * SPW];  // the planes of half A (0) and B (1) this warp's S-boxes write
 #pragma unroll
   for (int h = 0; h < 2; ++h)
 #pragma unroll
-    for (int o = 0; o < 4; ++o) H[h][o] = st[own[h][o]];
+    for (int o = 0; o < 4 * SPW; ++o) H[h][o] = st[own[h][o]];
   // stage s round rr updates A iff (rr + s) is even: stages 0 and 2
   // run (A, B) pairs, stage 1 (B, A) pairs.  Updating A reads half B (IN = 1).
 #pragma unroll
@@ -834,14 +859,14 @@ __device__ __forceinline__ void split_rounds(int G_, uint32_t* st, const SplitRo
 #pragma unroll 1
     for (int rr = 0; rr < 16; rr += 2) {
       const int r = 16 * stage + rr;
-      if (stage & 1) split_round<0>(G, st, win, own, H, S, K);
-      else split_round<1>(G, st, win, own, H, S, K);
+      if (stage & 1) split_round<SPW, 0>(G, st, win, own, H, S, K);
+      else split_round<SPW, 1>(G, st, win, own, H, S, K);
       split_keys(ks, r + 1, c, S, K);
-      team_sync();
-      if (stage & 1) split_round<1>(G, st, win, own, H, S, K);
-      else split_round<0>(G, st, win, own, H, S, K);
+      team_sync<SPW>();
+      if (stage & 1) split_round<SPW, 1>(G, st, win, own, H, S, K);
+      else split_round<SPW, 0>(G, st, win, own, H, S, K);
       if (r + 2 < 16 * NSTAGES) split_keys(ks, r + 2, c, S, K);
-      team_sync();
+      team_sync<SPW>();
     }
   }
 }
@@ -853,46 +878,56 @@ __device__ __forceinline__ void split_rounds(int G_, uint32_t* st, const SplitRo
 // is converged (inside it, every warp shuffle got a divergence fallback and the
 // specialised kernel grew to 220 KB of code, slower than the dispatching one from
 // 2^17 blocks on).
-template <int NSTAGES, bool SPEC>
+template <int SPW, int NSTAGES, bool SPEC>
 __device__ __forceinline__ void split_body(int G, const uint2* in, uint2* out, size_t nblocks, uint32_t* st,
-                                           const SplitRoundKeys (&ks)[16 * NSTAGES], unsigned lane, uint32_t c) {
+                                           const SplitRoundKeys<SPW> (&ks)[16 * NSTAGES], unsigned lane, uint32_t c) {
   const size_t ntiles = (nblocks + kGroupBlocks - 1) / kGroupBlocks;
   for (size_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const size_t base = tile * kGroupBlocks;
-    // load: warp G takes groups 4G..4G+3 (32 consecutive blocks each)
+    // load: warp G takes groups 4kG..4kG+4k-1, k = SPW (32 consecutive blocks each)
 #pragma unroll
-    for (int qq = 0; qq < 4; ++qq) {
-      const int q = 4 * G + qq;
+    for (int qq = 0; qq < 4 * SPW; ++qq) {
+      const int q = 4 * SPW * G + qq;
       const size_t b = base + 32 * q + lane;
       const uint2 v = b < nblocks ? __ldcs(in + b) : make_uint2(0u, 0u);
       st[lane * kStride + q] = warp_transpose32(v.x, lane);  // plane `lane` of group q
       st[(32 + lane) * kStride + q] = warp_transpose32(v.y, lane);
     }
     if (SPEC) {
-      switch (G) {  // a constant S-box index per case: split_rounds is inlined and specialised
-        case 0: split_rounds<NSTAGES, 0>(G, st, ks, lane, c); break;
-        case 1: split_rounds<NSTAGES, 1>(G, st, ks, lane, c); break;
-        case 2: split_rounds<NSTAGES, 2>(G, st, ks, lane, c); break;
-        case 3: split_rounds<NSTAGES, 3>(G, st, ks, lane, c); break;
-        case 4: split_rounds<NSTAGES, 4>(G, st, ks, lane, c); break;
-        case 5: split_rounds<NSTAGES, 5>(G, st, ks, lane, c); break;
-        case 6: split_rounds<NSTAGES, 6>(G, st, ks, lane, c); break;
-        default: split_rounds<NSTAGES, 7>(G, st, ks, lane, c); break;
+      // a constant warp index per case: split_rounds is inlined and specialised
+      if constexpr (SPW == 1) {
+        switch (G) {
+          case 0: split_rounds<SPW, NSTAGES, 0>(G, st, ks, lane, c); break;
+          case 1: split_rounds<SPW, NSTAGES, 1>(G, st, ks, lane, c); break;
+          case 2: split_rounds<SPW, NSTAGES, 2>(G, st, ks, lane, c); break;
+          case 3: split_rounds<SPW, NSTAGES, 3>(G, st, ks, lane, c); break;
+          case 4: split_rounds<SPW, NSTAGES, 4>(G, st, ks, lane, c); break;
+          case 5: split_rounds<SPW, NSTAGES, 5>(G, st, ks, lane, c); break;
+          case 6: split_rounds<SPW, NSTAGES, 6>(G, st, ks, lane, c); break;
+          default: split_rounds<SPW, NSTAGES, 7>(G, st, ks, lane, c); break;
+        }
+      } else {
+        switch (G) {
+          case 0: split_rounds<SPW, NSTAGES, 0>(G, st, ks, lane, c); break;
+          case 1: split_rounds<SPW, NSTAGES, 1>(G, st, ks, lane, c); break;
+          case 2: split_rounds<SPW, NSTAGES, 2>(G, st, ks, lane, c); break;
+          default: split_rounds<SPW, NSTAGES, 3>(G, st, ks, lane, c); break;
+        }
       }
       __syncwarp();  // converged again (keeps the store's shuffles free of divergence fallbacks)
     } else {
-      split_rounds<NSTAGES, -1>(G, st, ks, lane, c);
+      split_rounds<SPW, NSTAGES, -1>(G, st, ks, lane, c);
     }
-    // FP (renaming) + store: warp G writes groups 4G..4G+3
+    // FP (renaming) + store: warp G writes the groups it loaded
 #pragma unroll
-    for (int qq = 0; qq < 4; ++qq) {
-      const int q = 4 * G + qq;
+    for (int qq = 0; qq < 4 * SPW; ++qq) {
+      const int q = 4 * SPW * G + qq;
       const uint32_t wx = warp_transpose32(st[tdes_gen::kOutSrc[lane] * kStride + q], lane);
       const uint32_t wy = warp_transpose32(st[tdes_gen::kOutSrc[32 + lane] * kStride + q], lane);
       const size_t b = base + 32 * q + lane;
       if (b < nblocks) __stcs(out + b, make_uint2(wx, wy));
     }
-    team_sync();
+    team_sync<SPW>();
   }
 }
 
@@ -902,26 +937,29 @@ __device__ __forceinline__ void split_body(int G, const uint2* in, uint2* out, s
 // split size: 128 tiles (C1) 14.2 -> 12.3 us back to back, 27.8 -> 23.4 us single
 // (profiles/r02/split_spec_ab.txt), so auto mode always uses it; the dispatching
 // variant stays as a -DTDES_SPLIT_SPEC_MAX=<tiles> experiment switch.
-template <int NSTAGES, bool SPEC>
-__global__ void __launch_bounds__(kSplitThreads)
+template <int NSTAGES, int SPW, bool SPEC>
+__global__ void __launch_bounds__(kSplitThreads<SPW>)
 tdes_split_kernel(const uint2* in, uint2* out, size_t nblocks,
                   const __grid_constant__ RoundKeys<16 * NSTAGES> mk, uint32_t c) {
   __shared__ uint32_t st[64 * kStride];
-  __shared__ SplitKeys<16 * NSTAGES> ks;
+  __shared__ SplitKeys<SPW, 16 * NSTAGES> ks;
   const unsigned lane = threadIdx.x & 31u;
-  const int g = threadIdx.x >> 5;  // this warp's S-box
+  const int g = threadIdx.x >> 5;  // this warp: S-boxes SPW*g .. SPW*g + SPW - 1
   // this warp's 6 subkey bits per round (bit 47 - b of the packed subkey = E position b)
   for (int r = lane; r < 16 * NSTAGES; r += 32) {
-    const uint32_t kb = (uint32_t)(mk.k[r] >> (42 - 6 * g)) & 63u;
 #pragma unroll
-    for (int i = 0; i < 6; ++i) {
-      const uint32_t k = 0u - ((kb >> (5 - i)) & 1u);
-      ks.r[g][r].s[i] = k | 1u;
-      ks.r[g][r].k[i] = k;
+    for (int j = 0; j < SPW; ++j) {
+      const uint32_t kb = (uint32_t)(mk.k[r] >> (42 - 6 * (SPW * g + j))) & 63u;
+#pragma unroll
+      for (int i = 0; i < 6; ++i) {
+        const uint32_t k = 0u - ((kb >> (5 - i)) & 1u);
+        ks.r[g][r].s[6 * j + i] = k | 1u;
+        ks.r[g][r].k[6 * j + i] = k;
+      }
     }
   }
   __syncwarp();
-  split_body<NSTAGES, SPEC>(g, in, out, nblocks, st, ks.r[g], lane, c);
+  split_body<SPW, NSTAGES, SPEC>(g, in, out, nblocks, st, ks.r[g], lane, c);
 }
 
 // ------------------------------------------------------------ launching ---
@@ -979,7 +1017,14 @@ constexpr size_t kSplitMaxTiles = 296;
 #ifndef TDES_SPLIT_SPEC_MAX
 #define TDES_SPLIT_SPEC_MAX 296
 #endif
-constexpr size_t kSplitSpecMaxTiles = TDES_SPLIT_SPEC_MAX;  // the S-box-specialised split kernel (tdes_split_kernel<., true>)
+constexpr size_t kSplitSpecMaxTiles = TDES_SPLIT_SPEC_MAX;  // the S-box-specialised split kernel (tdes_split_kernel<., ., true>)
+// Teams of 4 warps with two S-boxes each (SPW = 2) from this many tiles on, teams of
+// 8 with one below: measured (B200, back to back) <= 16 tiles 10.3 vs 11.2-13.6 us,
+// 128 tiles 12.3 both, 256 tiles 16.4 vs 14.7 us (profiles/r02/split_spw_ab.txt).
+#ifndef TDES_SPLIT_SPW2_MIN
+#define TDES_SPLIT_SPW2_MIN 149
+#endif
+constexpr size_t kSplitSpw2MinTiles = TDES_SPLIT_SPW2_MIN;
 // Auto mode uses the throughput kernel whose s operands stay in the launch
 // parameters (mode 1) above kSplitMaxTiles.  (Until its prologue expanded k and d
 // on the device and issued the first tile's TMA copy before that expansion, the
@@ -1116,12 +1161,20 @@ int launch(const uint32_t (*masks)[48], const void* in, void* out, size_t nblock
     const size_t cap = (size_t)num_sms(dev) * 8u;  // up to 8 teams per SM
     const unsigned sgrid = (unsigned)(ngroups < cap ? ngroups : cap);
     const RoundKeys<16 * NSTAGES>& ms = cached_rkeys<NSTAGES>(masks);
-    if (ngroups <= kSplitSpecMaxTiles)
-      tdes_split_kernel<NSTAGES, true><<<sgrid, kSplitThreads, 0, stream>>>(
-          static_cast<const uint2*>(in), static_cast<uint2*>(out), nblocks, ms, kMulhiC);
-    else
-      tdes_split_kernel<NSTAGES, false><<<sgrid, kSplitThreads, 0, stream>>>(
-          static_cast<const uint2*>(in), static_cast<uint2*>(out), nblocks, ms, kMulhiC);
+    const uint2* pin = static_cast<const uint2*>(in);
+    uint2* pout = static_cast<uint2*>(out);
+    const bool spec = ngroups <= kSplitSpecMaxTiles;
+    if (ngroups < kSplitSpw2MinTiles) {
+      if (spec)
+        tdes_split_kernel<NSTAGES, 1, true><<<sgrid, kSplitThreads<1>, 0, stream>>>(pin, pout, nblocks, ms, kMulhiC);
+      else
+        tdes_split_kernel<NSTAGES, 1, false><<<sgrid, kSplitThreads<1>, 0, stream>>>(pin, pout, nblocks, ms, kMulhiC);
+    } else {
+      if (spec)
+        tdes_split_kernel<NSTAGES, 2, true><<<sgrid, kSplitThreads<2>, 0, stream>>>(pin, pout, nblocks, ms, kMulhiC);
+      else
+        tdes_split_kernel<NSTAGES, 2, false><<<sgrid, kSplitThreads<2>, 0, stream>>>(pin, pout, nblocks, ms, kMulhiC);
+    }
     e = cudaGetLastError();
     return e == cudaSuccess ? TDES_OK : cuda_fail(e);
   }
