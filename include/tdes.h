@@ -83,7 +83,7 @@ int tdes_key_schedule(const uint8_t k1[8], const uint8_t k2[8], const uint8_t k3
  *           subkeys, which each CTA expands into its key operands on the device,
  *           plus the uniform-path s operands), so *s may be freed or changed as
  *           soon as the call returns.
- * Kernel choice (automatic, by launch size in 1024-block tiles): <= 296 tiles the
+ * Kernel choice (automatic, by launch size in 1024-block tiles): <= 384 tiles the
  * S-box-split latency kernel, above that the throughput kernel (tdes_ecb_crypt_mode
  * in tdes_bench.h forces one).  All produce identical output.
  *   in,out  device pointers (current device), 8-byte aligned; in == out (in

@@ -1013,9 +1013,9 @@ int check_buffers(const void* in, const void* out, size_t nblocks) {
 
 // Auto mode: the split (latency) kernel for launches of at most this many
 // 1024-block tiles, the throughput kernel above (measured crossover).
-constexpr size_t kSplitMaxTiles = 296;
+constexpr size_t kSplitMaxTiles = 384;
 #ifndef TDES_SPLIT_SPEC_MAX
-#define TDES_SPLIT_SPEC_MAX 296
+#define TDES_SPLIT_SPEC_MAX 384
 #endif
 constexpr size_t kSplitSpecMaxTiles = TDES_SPLIT_SPEC_MAX;  // the S-box-specialised split kernel (tdes_split_kernel<., ., true>)
 // Teams of 4 warps with two S-boxes each (SPW = 2) from this many tiles on, teams of

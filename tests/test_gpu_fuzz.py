@@ -1,8 +1,8 @@
 """Seeded randomized parity: the CUDA path against the oracle on random configurations.
 
 Each case draws a size (ragged: inside a lane's 32 blocks, a warp's 1024-block tile,
-the split kernel's 296-tile limit and beyond), an alignment (16-byte: TMA/LDG.128
-path; 8-byte: LDG.64 path), a keying (3-key, 2-key K1 = K3, 1-key, random keys with
+the split kernel's team-size switch at 149 tiles and its 384-tile limit, and beyond),
+an alignment (16-byte: TMA/LDG.128 path; 8-byte: LDG.64 path), a keying (3-key, 2-key K1 = K3, 1-key, random keys with
 weak and semi-weak keys mixed in), a direction, a kernel (auto, throughput with
 host- or device-expanded key operands, S-box split) and in-place or not, and compares
 every block with the oracle (PAPER.md:82-84 per block; P:138 ECB independence).
@@ -20,7 +20,8 @@ pytestmark = pytest.mark.gpu
 # weak and semi-weak DES keys (FIPS 74 / SP 800-67 list)
 SPECIAL = ["0101010101010101", "FEFEFEFEFEFEFEFE", "E0E0E0E0F1F1F1F1", "1F1F1F1F0E0E0E0E",
            "011F011F010E010E", "1F011F010E010E01", "01E001E001F101F1", "E001E001F101F101"]
-SIZES = [1, 7, 31, 32, 33, 1000, 1023, 1024, 1025, 4095, 30001, 296 * 1024 - 1, 296 * 1024 + 1, 400_000]
+SIZES = [1, 7, 31, 32, 33, 1000, 1023, 1024, 1025, 4095, 30001, 148 * 1024 + 1, 384 * 1024 - 1, 384 * 1024 + 1,
+         400_000]
 
 
 @pytest.fixture(scope="module")
