@@ -737,10 +737,16 @@ tdes_ecb_kernel(const uint2* in, uint2* out, size_t nblocks,
 // round.  Transposes are lane-parallel (5 shuffle butterfly stages).  From 149
 // tiles on (more than one team per SM) teams of 4 warps run two adjacent S-boxes
 // per warp (SPW = 2): two independent S-box chains per warp, one warp per SMSP.
-// SPW = S-boxes per warp: 1 = a team of 8 warps (one S-box each), 2 = a team of
-// 4 warps (two adjacent S-boxes each); the launcher picks by size.
-template <int SPW>
-constexpr int kSplitThreads = 256 / SPW;  // one team
+// WPT = warps per team: 8 = one S-box per warp; 4 = two adjacent S-boxes per warp
+// (two independent S-box chains per warp); 16 = half an S-box per warp (outputs
+// 0-1 or 2-3: the compiler drops the gates only the other pair needs).  The
+// launcher picks by size.
+template <int WPT>
+constexpr int kSplitThreads = 32 * WPT;  // one team
+template <int WPT>
+constexpr int kBoxesPerWarp = WPT >= 8 ? 1 : 8 / WPT;
+template <int WPT>
+constexpr int kOutsPerBox = WPT == 16 ? 2 : 4;
 constexpr int kStride = 33;
 
 // 32x32 bit transpose across a warp: lane i holds row i on entry; on exit lane
@@ -763,95 +769,121 @@ __device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, unsigned lane) 
   return x;
 }
 
-// Team barrier.  bar.sync counts arriving threads per barrier id, so the eight
-// warps may reach it from the different S-box cases of sbox_by_index.
-template <int SPW>
+// Team barrier.  bar.sync counts arriving threads per barrier id, so the warps
+// may reach it from the different S-box cases of the specialised kernel.
+template <int WPT>
 __device__ __forceinline__ void team_sync() {
-  asm volatile("bar.sync 0, %0;" ::"n"(kSplitThreads<SPW>) : "memory");
+  asm volatile("bar.sync 0, %0;" ::"n"(kSplitThreads<WPT>) : "memory");
 }
 
 // Per-warp key material for the split kernel: s = k | 1 (+1 / -1) and k (0 / ~0)
-// of this warp's S-box's 6 key bits for every round (48 bytes per round: three
-// LDS.128 and no arithmetic between the load and the round's IMADs, so the loads
-// issued before a barrier complete while the team waits).  Measured against
-// loading s only and rebuilding k = mulhi(c, s) before the barrier: see DESIGN.md §6.
-template <int SPW>
+// of the 6 key bits of each of this warp's S-boxes for every round (48 bytes per
+// S-box and round: LDS.128s and no arithmetic between the load and the round's
+// IMADs, so the loads issued before a barrier complete while the team waits).
+// Measured against loading s only and rebuilding k = mulhi(c, s) before the
+// barrier: see DESIGN.md §6.
+template <int NB>
 struct alignas(16) SplitRoundKeys {
-  uint32_t s[6 * SPW], k[6 * SPW];
+  uint32_t s[6 * NB], k[6 * NB];
 };
-template <int SPW, int NROUNDS>
+template <int WPT, int NROUNDS>
 struct SplitKeys {
-  SplitRoundKeys<SPW> r[8 / SPW][NROUNDS];
+  SplitRoundKeys<kBoxesPerWarp<WPT>> r[WPT][NROUNDS];
 };
 
-// One round of the split kernel for S-box G: read the E-window of half IN from
-// shared memory, key XOR (s, k prefetched a round earlier), S-box, publish the 4
-// planes of the other half this warp owns.
-template <int SPW, int IN>
-__device__ __forceinline__ void split_round(int G, uint32_t* st, const int (&win)[2][6 * SPW],
-                                            const int (&own)[2][4 * SPW], uint32_t (&H)[2][4 * SPW],
-                                            const uint32_t (&S)[6 * SPW], const uint32_t (&K)[6 * SPW]) {
-  constexpr int OUT = 1 - IN;
+// S-box j of warp G, and the first of its outputs the warp owns.
+template <int WPT>
+__device__ __forceinline__ int split_box(int G, int j) {
+  return WPT == 16 ? G >> 1 : kBoxesPerWarp<WPT> * G + j;
+}
+template <int WPT>
+__device__ __forceinline__ int split_out0(int G) {
+  return WPT == 16 ? 2 * (G & 1) : 0;
+}
+
+// One round of the split kernel for warp G: read the E-windows of half IN from
+// shared memory, key XOR (s, k prefetched a round earlier), the S-box(es), publish
+// the planes of the other half this warp owns.
+template <int WPT, int IN>
+__device__ __forceinline__ void split_round(int G, uint32_t* st, const int (&win)[2][6 * kBoxesPerWarp<WPT>],
+                                            const int (&own)[2][kBoxesPerWarp<WPT> * kOutsPerBox<WPT>],
+                                            uint32_t (&H)[2][kBoxesPerWarp<WPT> * kOutsPerBox<WPT>],
+                                            const uint32_t (&S)[6 * kBoxesPerWarp<WPT>],
+                                            const uint32_t (&K)[6 * kBoxesPerWarp<WPT>]) {
+  constexpr int OUT = 1 - IN, NB = kBoxesPerWarp<WPT>, NO = kOutsPerBox<WPT>;
 #pragma unroll
-  for (int j = 0; j < SPW; ++j) {
+  for (int j = 0; j < NB; ++j) {
     uint32_t x[6];
 #pragma unroll
     for (int i = 0; i < 6; ++i) x[i] = tdes_gen::kxor<false>(st[win[IN][6 * j + i]], S[6 * j + i], K[6 * j + i], 0u);
-    tdes_gen::sbox_by_index(SPW * G + j, x[0], x[1], x[2], x[3], x[4], x[5], H[OUT][4 * j], H[OUT][4 * j + 1],
-                            H[OUT][4 * j + 2], H[OUT][4 * j + 3]);
+    if constexpr (NO == 4) {
+      tdes_gen::sbox_by_index(split_box<WPT>(G, j), x[0], x[1], x[2], x[3], x[4], x[5], H[OUT][4 * j],
+                              H[OUT][4 * j + 1], H[OUT][4 * j + 2], H[OUT][4 * j + 3]);
+    } else {  // half an S-box: the unused pair's results (and gates only they need) are dropped
+      uint32_t u0 = 0u, u1 = 0u;
+      if (split_out0<WPT>(G) == 0)
+        tdes_gen::sbox_by_index(split_box<WPT>(G, j), x[0], x[1], x[2], x[3], x[4], x[5], H[OUT][0], H[OUT][1], u0,
+                                u1);
+      else
+        tdes_gen::sbox_by_index(split_box<WPT>(G, j), x[0], x[1], x[2], x[3], x[4], x[5], u0, u1, H[OUT][0],
+                                H[OUT][1]);
+    }
   }
 #pragma unroll
-  for (int o = 0; o < 4 * SPW; ++o) st[own[OUT][o]] = H[OUT][o];
+  for (int o = 0; o < NB * NO; ++o) st[own[OUT][o]] = H[OUT][o];
 }
 
 // Load round r's key operands of this warp (off the critical path: issued before
 // the barrier that ends round r - 1).
-template <int SPW, int NROUNDS>
-__device__ __forceinline__ void split_keys(const SplitRoundKeys<SPW> (&ks)[NROUNDS], int r, uint32_t,
-                                           uint32_t (&S)[6 * SPW], uint32_t (&K)[6 * SPW]) {
+template <int NB, int NROUNDS>
+__device__ __forceinline__ void split_keys(const SplitRoundKeys<NB> (&ks)[NROUNDS], int r, uint32_t,
+                                           uint32_t (&S)[6 * NB], uint32_t (&K)[6 * NB]) {
   const uint4* v = reinterpret_cast<const uint4*>(&ks[r]);
-  uint32_t w[12 * SPW];
+  uint32_t w[12 * NB];
 #pragma unroll
-  for (int q = 0; q < 3 * SPW; ++q) {
+  for (int q = 0; q < 3 * NB; ++q) {
     const uint4 a = v[q];
     w[4 * q] = a.x; w[4 * q + 1] = a.y; w[4 * q + 2] = a.z; w[4 * q + 3] = a.w;
   }
 #pragma unroll
-  for (int i = 0; i < 6 * SPW; ++i) {
+  for (int i = 0; i < 6 * NB; ++i) {
     S[i] = w[i];
-    K[i] = w[6 * SPW + i];
+    K[i] = w[6 * NB + i];
   }
 }
 
-// The 48 rounds of one tile for the warp that evaluates S-box G (warp-uniform;
-// GC >= 0: G = GC known at compile time, the S-box-specialised variant).  The
-// rounds run in (A, B) / (B, A) pairs, so no per-round branch picks the half; the
-// key operands of the next round are loaded before each barrier.  Measured (B200,
-// back-to-back 3DES launches): 16.5 -> 14.4 us for 1-16 tiles, 16.5 -> 14.5 us at
-// 2^17 blocks, 20.5 -> 18.5 us at 2^18.
-template <int SPW, int NSTAGES, int GC>
-__device__ __forceinline__ void split_rounds(int G_, uint32_t* st, const SplitRoundKeys<SPW> (&ks)[16 * NSTAGES],
+// The 48 rounds of one tile for warp G (warp-uniform; GC >= 0: G = GC known at
+// compile time, the S-box-specialised variant).  The rounds run in (A, B) / (B, A)
+// pairs, so no per-round branch picks the half; the key operands of the next round
+// are loaded before each barrier.  Measured (B200, back-to-back 3DES launches):
+// 16.5 -> 14.4 us for 1-16 tiles, 16.5 -> 14.5 us at 2^17 blocks, 20.5 -> 18.5 us at
+// 2^18.
+template <int WPT, int NSTAGES, int GC>
+__device__ __forceinline__ void split_rounds(int G_, uint32_t* st,
+                                             const SplitRoundKeys<kBoxesPerWarp<WPT>> (&ks)[16 * NSTAGES],
                                              unsigned lane, uint32_t c) {
-  const int G = GC >= 0 ? GC : G_;   // this warp: S-boxes SPW*G .. SPW*G + SPW - 1
-  int win[2][6 * SPW], own[2][4 * SPW];
+  constexpr int NB = kBoxesPerWarp<WPT>, NO = kOutsPerBox<WPT>;
+  const int G = GC >= 0 ? GC : G_;
+  int win[2][6 * NB], own[2][NB * NO];
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
 #pragma unroll
-    for (int j = 0; j < SPW; ++j) {
+    for (int j = 0; j < NB; ++j) {
+      const int g = split_box<WPT>(G, j);
 #pragma unroll
-      for (int i = 0; i < 6; ++i) win[h][6 * j + i] = tdes_gen::kWin[h][SPW * G + j][i] * kStride + lane;
+      for (int i = 0; i < 6; ++i) win[h][6 * j + i] = tdes_gen::kWin[h][g][i] * kStride + lane;
 #pragma unroll
-      for (int o = 0; o < 4; ++o) own[h][4 * j + o] = tdes_gen::kOwn[h][SPW * G + j][o] * kStride + lane;
+      for (int o = 0; o < NO; ++o) own[h][NO * j + o] = tdes_gen::kOwn[h][g][split_out0<WPT>(G) + o] * kStride + lane;
     }
   }
-  uint32_t S[6 * SPW], K[6 * SPW];
+  uint32_t S[6 * NB], K[6 * NB];
   split_keys(ks, 0, c, S, K);
-  team_sync<SPW>();
-  uint32_t H[2][4 * SPW];  // the planes of half A (0) and B (1) this warp's S-boxes write
+  team_sync<WPT>();
+  uint32_t H[2][NB * NO];  // the planes of half A (0) and B (1) this warp writes
 #pragma unroll
   for (int h = 0; h < 2; ++h)
 #pragma unroll
-    for (int o = 0; o < 4 * SPW; ++o) H[h][o] = st[own[h][o]];
+    for (int o = 0; o < NB * NO; ++o) H[h][o] = st[own[h][o]];
   // stage s round rr updates A iff (rr + s) is even: stages 0 and 2
   // run (A, B) pairs, stage 1 (B, A) pairs.  Updating A reads half B (IN = 1).
 #pragma unroll
@@ -859,75 +891,70 @@ __device__ __forceinline__ void split_rounds(int G_, uint32_t* st, const SplitRo
 #pragma unroll 1
     for (int rr = 0; rr < 16; rr += 2) {
       const int r = 16 * stage + rr;
-      if (stage & 1) split_round<SPW, 0>(G, st, win, own, H, S, K);
-      else split_round<SPW, 1>(G, st, win, own, H, S, K);
+      if (stage & 1) split_round<WPT, 0>(G, st, win, own, H, S, K);
+      else split_round<WPT, 1>(G, st, win, own, H, S, K);
       split_keys(ks, r + 1, c, S, K);
-      team_sync<SPW>();
-      if (stage & 1) split_round<SPW, 1>(G, st, win, own, H, S, K);
-      else split_round<SPW, 0>(G, st, win, own, H, S, K);
+      team_sync<WPT>();
+      if (stage & 1) split_round<WPT, 1>(G, st, win, own, H, S, K);
+      else split_round<WPT, 0>(G, st, win, own, H, S, K);
       if (r + 2 < 16 * NSTAGES) split_keys(ks, r + 2, c, S, K);
-      team_sync<SPW>();
+      team_sync<WPT>();
     }
+  }
+}
+
+// The specialised rounds: a constant warp index per case (split_rounds is inlined
+// and specialised), cases 0 .. WPT-1.
+template <int WPT, int NSTAGES, int C0>
+__device__ __forceinline__ void split_rounds_spec(int G, uint32_t* st,
+                                                  const SplitRoundKeys<kBoxesPerWarp<WPT>> (&ks)[16 * NSTAGES],
+                                                  unsigned lane, uint32_t c) {
+  if constexpr (C0 < WPT) {
+    if (G == C0) split_rounds<WPT, NSTAGES, C0>(G, st, ks, lane, c);
+    else split_rounds_spec<WPT, NSTAGES, C0 + 1>(G, st, ks, lane, c);
   }
 }
 
 // The tile loop of warp G: load (lane-parallel transposes into the shared round
 // state), the rounds, store.  SPEC: the rounds run in a copy specialised for the
-// warp's S-box (no per-round dispatch).  Only the rounds are specialised: the load
-// and store stay outside the per-S-box switch, where the compiler knows the warp
-// is converged (inside it, every warp shuffle got a divergence fallback and the
-// specialised kernel grew to 220 KB of code, slower than the dispatching one from
-// 2^17 blocks on).
-template <int SPW, int NSTAGES, bool SPEC>
+// warp's S-box(es) (no per-round dispatch).  Only the rounds are specialised: the
+// load and store stay outside the per-warp dispatch, where the compiler knows the
+// warp is converged (inside it, every warp shuffle got a divergence fallback and
+// the specialised kernel grew to 220 KB of code, slower than the dispatching one
+// from 2^17 blocks on).
+template <int WPT, int NSTAGES, bool SPEC>
 __device__ __forceinline__ void split_body(int G, const uint2* in, uint2* out, size_t nblocks, uint32_t* st,
-                                           const SplitRoundKeys<SPW> (&ks)[16 * NSTAGES], unsigned lane, uint32_t c) {
+                                           const SplitRoundKeys<kBoxesPerWarp<WPT>> (&ks)[16 * NSTAGES],
+                                           unsigned lane, uint32_t c) {
+  constexpr int QW = 32 / WPT;  // 32-block groups per warp in the load and store
   const size_t ntiles = (nblocks + kGroupBlocks - 1) / kGroupBlocks;
   for (size_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const size_t base = tile * kGroupBlocks;
-    // load: warp G takes groups 4kG..4kG+4k-1, k = SPW (32 consecutive blocks each)
+    // load: warp G takes groups QW*G .. QW*G + QW - 1 (32 consecutive blocks each)
 #pragma unroll
-    for (int qq = 0; qq < 4 * SPW; ++qq) {
-      const int q = 4 * SPW * G + qq;
+    for (int qq = 0; qq < QW; ++qq) {
+      const int q = QW * G + qq;
       const size_t b = base + 32 * q + lane;
       const uint2 v = b < nblocks ? __ldcs(in + b) : make_uint2(0u, 0u);
       st[lane * kStride + q] = warp_transpose32(v.x, lane);  // plane `lane` of group q
       st[(32 + lane) * kStride + q] = warp_transpose32(v.y, lane);
     }
     if (SPEC) {
-      // a constant warp index per case: split_rounds is inlined and specialised
-      if constexpr (SPW == 1) {
-        switch (G) {
-          case 0: split_rounds<SPW, NSTAGES, 0>(G, st, ks, lane, c); break;
-          case 1: split_rounds<SPW, NSTAGES, 1>(G, st, ks, lane, c); break;
-          case 2: split_rounds<SPW, NSTAGES, 2>(G, st, ks, lane, c); break;
-          case 3: split_rounds<SPW, NSTAGES, 3>(G, st, ks, lane, c); break;
-          case 4: split_rounds<SPW, NSTAGES, 4>(G, st, ks, lane, c); break;
-          case 5: split_rounds<SPW, NSTAGES, 5>(G, st, ks, lane, c); break;
-          case 6: split_rounds<SPW, NSTAGES, 6>(G, st, ks, lane, c); break;
-          default: split_rounds<SPW, NSTAGES, 7>(G, st, ks, lane, c); break;
-        }
-      } else {
-        switch (G) {
-          case 0: split_rounds<SPW, NSTAGES, 0>(G, st, ks, lane, c); break;
-          case 1: split_rounds<SPW, NSTAGES, 1>(G, st, ks, lane, c); break;
-          case 2: split_rounds<SPW, NSTAGES, 2>(G, st, ks, lane, c); break;
-          default: split_rounds<SPW, NSTAGES, 3>(G, st, ks, lane, c); break;
-        }
-      }
+      split_rounds_spec<WPT, NSTAGES, 0>(G, st, ks, lane, c);
       __syncwarp();  // converged again (keeps the store's shuffles free of divergence fallbacks)
     } else {
-      split_rounds<SPW, NSTAGES, -1>(G, st, ks, lane, c);
+      split_rounds<WPT, NSTAGES, -1>(G, st, ks, lane, c);
     }
     // FP (renaming) + store: warp G writes the groups it loaded
 #pragma unroll
-    for (int qq = 0; qq < 4 * SPW; ++qq) {
-      const int q = 4 * SPW * G + qq;
+    for (int qq = 0; qq < QW; ++qq) {
+      const int q = QW * G + qq;
       const uint32_t wx = warp_transpose32(st[tdes_gen::kOutSrc[lane] * kStride + q], lane);
       const uint32_t wy = warp_transpose32(st[tdes_gen::kOutSrc[32 + lane] * kStride + q], lane);
       const size_t b = base + 32 * q + lane;
       if (b < nblocks) __stcs(out + b, make_uint2(wx, wy));
     }
-    team_sync<SPW>();
+    team_sync<WPT>();
   }
 }
 
@@ -937,19 +964,21 @@ __device__ __forceinline__ void split_body(int G, const uint2* in, uint2* out, s
 // split size: 128 tiles (C1) 14.2 -> 12.3 us back to back, 27.8 -> 23.4 us single
 // (profiles/r02/split_spec_ab.txt), so auto mode always uses it; the dispatching
 // variant stays as a -DTDES_SPLIT_SPEC_MAX=<tiles> experiment switch.
-template <int NSTAGES, int SPW, bool SPEC>
-__global__ void __launch_bounds__(kSplitThreads<SPW>)
+template <int NSTAGES, int WPT, bool SPEC>
+__global__ void __launch_bounds__(kSplitThreads<WPT>)
 tdes_split_kernel(const uint2* in, uint2* out, size_t nblocks,
                   const __grid_constant__ RoundKeys<16 * NSTAGES> mk, uint32_t c) {
+  constexpr int NB = kBoxesPerWarp<WPT>;
   __shared__ uint32_t st[64 * kStride];
-  __shared__ SplitKeys<SPW, 16 * NSTAGES> ks;
+  __shared__ SplitKeys<WPT, 16 * NSTAGES> ks;
   const unsigned lane = threadIdx.x & 31u;
-  const int g = threadIdx.x >> 5;  // this warp: S-boxes SPW*g .. SPW*g + SPW - 1
-  // this warp's 6 subkey bits per round (bit 47 - b of the packed subkey = E position b)
+  const int g = threadIdx.x >> 5;  // this warp
+  // the 6 subkey bits of each of this warp's S-boxes per round (bit 47 - b of the
+  // packed subkey = E position b)
   for (int r = lane; r < 16 * NSTAGES; r += 32) {
 #pragma unroll
-    for (int j = 0; j < SPW; ++j) {
-      const uint32_t kb = (uint32_t)(mk.k[r] >> (42 - 6 * (SPW * g + j))) & 63u;
+    for (int j = 0; j < NB; ++j) {
+      const uint32_t kb = (uint32_t)(mk.k[r] >> (42 - 6 * split_box<WPT>(g, j))) & 63u;
 #pragma unroll
       for (int i = 0; i < 6; ++i) {
         const uint32_t k = 0u - ((kb >> (5 - i)) & 1u);
@@ -959,7 +988,7 @@ tdes_split_kernel(const uint2* in, uint2* out, size_t nblocks,
     }
   }
   __syncwarp();
-  split_body<SPW, NSTAGES, SPEC>(g, in, out, nblocks, st, ks.r[g], lane, c);
+  split_body<WPT, NSTAGES, SPEC>(g, in, out, nblocks, st, ks.r[g], lane, c);
 }
 
 // ------------------------------------------------------------ launching ---
@@ -1025,6 +1054,11 @@ constexpr size_t kSplitSpecMaxTiles = TDES_SPLIT_SPEC_MAX;  // the S-box-special
 #define TDES_SPLIT_SPW2_MIN 149
 #endif
 constexpr size_t kSplitSpw2MinTiles = TDES_SPLIT_SPW2_MIN;
+// Team size below kSplitSpw2MinTiles (experiment switch: 8 or 16 warps).
+#ifndef TDES_SPLIT_SMALL_WPT
+#define TDES_SPLIT_SMALL_WPT 8
+#endif
+constexpr int kSplitSmallWpt = TDES_SPLIT_SMALL_WPT;
 // Auto mode uses the throughput kernel whose s operands stay in the launch
 // parameters (mode 1) above kSplitMaxTiles.  (Until its prologue expanded k and d
 // on the device and issued the first tile's TMA copy before that expansion, the
@@ -1166,14 +1200,16 @@ int launch(const uint32_t (*masks)[48], const void* in, void* out, size_t nblock
     const bool spec = ngroups <= kSplitSpecMaxTiles;
     if (ngroups < kSplitSpw2MinTiles) {
       if (spec)
-        tdes_split_kernel<NSTAGES, 1, true><<<sgrid, kSplitThreads<1>, 0, stream>>>(pin, pout, nblocks, ms, kMulhiC);
+        tdes_split_kernel<NSTAGES, kSplitSmallWpt, true><<<sgrid, kSplitThreads<kSplitSmallWpt>, 0, stream>>>(
+            pin, pout, nblocks, ms, kMulhiC);
       else
-        tdes_split_kernel<NSTAGES, 1, false><<<sgrid, kSplitThreads<1>, 0, stream>>>(pin, pout, nblocks, ms, kMulhiC);
+        tdes_split_kernel<NSTAGES, kSplitSmallWpt, false><<<sgrid, kSplitThreads<kSplitSmallWpt>, 0, stream>>>(
+            pin, pout, nblocks, ms, kMulhiC);
     } else {
       if (spec)
-        tdes_split_kernel<NSTAGES, 2, true><<<sgrid, kSplitThreads<2>, 0, stream>>>(pin, pout, nblocks, ms, kMulhiC);
+        tdes_split_kernel<NSTAGES, 4, true><<<sgrid, kSplitThreads<4>, 0, stream>>>(pin, pout, nblocks, ms, kMulhiC);
       else
-        tdes_split_kernel<NSTAGES, 2, false><<<sgrid, kSplitThreads<2>, 0, stream>>>(pin, pout, nblocks, ms, kMulhiC);
+        tdes_split_kernel<NSTAGES, 4, false><<<sgrid, kSplitThreads<4>, 0, stream>>>(pin, pout, nblocks, ms, kMulhiC);
     }
     e = cudaGetLastError();
     return e == cudaSuccess ? TDES_OK : cuda_fail(e);
