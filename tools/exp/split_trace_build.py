@@ -35,29 +35,29 @@ def patch(t: str) -> str:
     rhead = "  const int G = GC >= 0 ? GC : G_;"
     assert rhead in t
     t = t.replace(rhead, rhead + "\n  long long* tr = (blockIdx.x == 0 && lane == 0) ? &g_strace[G][0][0] : nullptr;\n  int ri = 0;", 1)
-    for old in ("      split_keys(ks, r + 1, c, S, K);\n      team_sync<SPW>();\n",
-                "      if (r + 2 < 16 * NSTAGES) split_keys(ks, r + 2, c, S, K);\n      team_sync<SPW>();\n"):
+    for old in ("      split_keys(ks, r + 1, c, S, K);\n      team_sync<WPT>();\n",
+                "      if (r + 2 < 16 * NSTAGES) split_keys(ks, r + 2, c, S, K);\n      team_sync<WPT>();\n"):
         assert old in t, old
-        new = old.replace("      team_sync<SPW>();\n",
-                          "      if (tr && ri < 100) tr[ri] = clock64();\n      team_sync<SPW>();\n"
+        new = old.replace("      team_sync<WPT>();\n",
+                          "      if (tr && ri < 100) tr[ri] = clock64();\n      team_sync<WPT>();\n"
                           "      if (tr && ri < 100) tr[100 + ri] = clock64();\n      ++ri;\n")
         t = t.replace(old, new, 1)
-    ph = [("  const unsigned lane = threadIdx.x & 31u;\n  const int g = threadIdx.x >> 5;  // this warp: S-boxes SPW*g .. SPW*g + SPW - 1\n",
+    ph = [("  const unsigned lane = threadIdx.x & 31u;\n  const int g = threadIdx.x >> 5;  // this warp\n",
            "  const bool ph0 = blockIdx.x == 0 && lane == 0;\n  if (ph0) g_sphase[g][0] = gt_now();\n"
            "  if (lane == 0 && g == 0 && blockIdx.x < 1024) g_scta[blockIdx.x][0] = gt_now();\n"),
-          ("  __syncwarp();\n  split_body<SPW, NSTAGES, SPEC>(", ""),
-          ("    if (SPEC) {\n      // a constant warp index per case", "PREFIX    if (tr && tile == blockIdx.x) g_sphase[G][2] = gt_now();\n"),
+          ("  __syncwarp();\n  split_body<WPT, NSTAGES, SPEC>(", ""),
+          ("    if (SPEC) {\n      split_rounds_spec", "PREFIX    if (tr && tile == blockIdx.x) g_sphase[G][2] = gt_now();\n"),
           ("    // FP (renaming) + store: warp G writes the groups it loaded\n", "    if (tr && tile == blockIdx.x) g_sphase[G][3] = gt_now();\n"),
-          ("    team_sync<SPW>();\n  }\n}\n", "    if (tr && tile == blockIdx.x) g_sphase[G][4] = gt_now();\n")]
+          ("    team_sync<WPT>();\n  }\n}\n", "    if (tr && tile == blockIdx.x) g_sphase[G][4] = gt_now();\n")]
     for anchor, ins in ph:
         assert anchor in t, anchor
         if anchor.startswith("  __syncwarp();\n  split_body"):
-            t = t.replace(anchor, "  __syncwarp();\n  if (ph0) g_sphase[g][1] = gt_now();\n  split_body<SPW, NSTAGES, SPEC>(", 1)
+            t = t.replace(anchor, "  __syncwarp();\n  if (ph0) g_sphase[g][1] = gt_now();\n  split_body<WPT, NSTAGES, SPEC>(", 1)
         elif ins.startswith("PREFIX"):
             t = t.replace(anchor, ins[len("PREFIX"):] + anchor, 1)
         else:
             t = t.replace(anchor, anchor + ins if not anchor.startswith("    team_sync") else ins + anchor, 1)
-    tail = "  split_body<SPW, NSTAGES, SPEC>(g, in, out, nblocks, st, ks.r[g], lane, c);\n}\n"
+    tail = "  split_body<WPT, NSTAGES, SPEC>(g, in, out, nblocks, st, ks.r[g], lane, c);\n}\n"
     assert tail in t
     t = t.replace(tail, tail[:-2] + "  if (ph0) g_sphase[g][5] = gt_now();\n"
                   "  if (lane == 0 && g == 0 && blockIdx.x < 1024) g_scta[blockIdx.x][1] = gt_now();\n}\n", 1)
