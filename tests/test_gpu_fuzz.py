@@ -87,3 +87,27 @@ def test_random_des_vs_oracle(tdes, case):
     fn = tdes.des_ecb_decrypt if decrypt else tdes.des_ecb_encrypt
     got = fn(_buffer(p, bool(rng.integers(2))), s).cpu().numpy()
     assert np.array_equal(got, oracle.tdes_ecb(k, k, k, p, decrypt=decrypt)), f"n={n} key={k} decrypt={decrypt}"
+
+
+@pytest.mark.parametrize("n", [3000, 200_001, 524_288 + 77])
+def test_alternating_key_schedules(tdes, n):
+    """The launch-operand caches (two entries per host thread, keyed by the key
+    material) must never serve a stale schedule: cycle through three schedules, both
+    directions, and a schedule modified in place between calls."""
+    rng = np.random.default_rng(n)
+    keysets = [tuple(synthetic.random_key(rng) for _ in range(3)) for _ in range(3)]
+    scheds = [tdes.key_schedule(*k) for k in keysets]
+    p = synthetic.random_blocks(rng, n)
+    x = torch.from_numpy(p).cuda()
+    for it in range(7):
+        i = (it * 2) % 3
+        dec = bool(it & 1)
+        got = (tdes.ecb_decrypt if dec else tdes.ecb_encrypt)(x, scheds[i]).cpu().numpy()
+        assert np.array_equal(got, oracle.tdes_ecb(*keysets[i], p, decrypt=dec)), (it, i, dec)
+    s = tdes.key_schedule(*keysets[0])
+    tdes.ecb_encrypt(x, s)
+    fresh = tdes.key_schedule(*keysets[1])
+    import ctypes
+    ctypes.memmove(ctypes.addressof(s), ctypes.addressof(fresh), ctypes.sizeof(s))  # same object, new keys
+    got = tdes.ecb_encrypt(x, s).cpu().numpy()
+    assert np.array_equal(got, oracle.tdes_ecb(*keysets[1], p))
