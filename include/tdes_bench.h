@@ -50,7 +50,9 @@ int tdes_lop3_peak(uint32_t *dev_sink, int grid, int cta, int iters, uint64_t *o
  *           kernel for small launches, the throughput kernel otherwise)
  *   mode 1  throughput kernel (32 blocks per thread, one warp per 1024-block tile;
  *           s operands in the launch parameters, k/d expanded on the device)
- *   mode 2  S-box-split latency kernel (8 warps per tile, one S-box per warp)
+ *   mode 2  S-box-split latency kernel (a team of warps per 1024-block tile: 8
+ *           warps with one S-box each below 149 tiles, 4 warps with two adjacent
+ *           S-boxes each from 149 tiles on)
  *   mode 3  throughput kernel with all key operands expanded on the device: the
  *           launch carries only the 48 packed 48-bit subkeys (384 B); every CTA
  *           expands them into every folded key operand, s included, in shared
