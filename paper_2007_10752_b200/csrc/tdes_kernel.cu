@@ -62,6 +62,11 @@ constexpr int kTileBlocks = kGroupBlocks * kWords;  // per warp
 #define TDES_ROUND_UNROLL 2
 #endif
 constexpr int kRoundUnroll3 = TDES_ROUND_UNROLL;
+// Two-round bodies per loop iteration of the single-DES round loop.
+#ifndef TDES_ROUND_UNROLL1
+#define TDES_ROUND_UNROLL1 1
+#endif
+constexpr int kRoundUnroll1 = TDES_ROUND_UNROLL1;
 // TMA-staged loads: each warp's next 8 KiB tile is fetched into a per-warp
 // shared-memory buffer by one cp.async.bulk (completion on a per-warp mbarrier)
 // while the warp computes the current tile, hiding the HBM latency at tile start.
@@ -438,7 +443,7 @@ __device__ __forceinline__ void crypt_tile(const uint2* in, uint2* out, size_t b
   // the instruction cache.  The middle stage starts on the half the first one
   // updated last, so at each stage boundary the halves swap
   // register roles and the same A-then-B body continues.
-  constexpr int kUnroll = NSTAGES == 3 ? kRoundUnroll3 : 1;
+  constexpr int kUnroll = NSTAGES == 3 ? kRoundUnroll3 : kRoundUnroll1;
   kv.fixup(P, 0, c);
 #pragma unroll kUnroll
   for (int r = 0; r < 16 * NSTAGES; r += 2) {
